@@ -224,7 +224,8 @@ class Alg1:
             u = x[: d * n2].reshape(d, n2)
             du = np.linalg.norm(u - w)
             w = u
-            if du <= self.picard_rtol * np.linalg.norm(u):
+            # C11: ||du||_2 <= rtol ||u||_2, or an absolute floor 1e-14 sqrt(N) for (near-)zero velocity
+            if du <= self.picard_rtol * np.linalg.norm(u) or du <= 1e-14 * np.sqrt(u.size):
                 self.picard_iters.append(it + 1)
                 return u, x[d * n2:]
         raise RuntimeError("Picard did not converge (C11)")

@@ -12,7 +12,8 @@ Each local problem is written in the paper's correction form: unknown e, with
 the bracketed coarse residual on the right-hand side, solved by SuperLU
 (scipy.sparse.linalg.splu).  Readings: C2 lag source (mode "composite" = B,
 "subdomain" = A), C4/C5 boundary data of e, C6 mean-zero multiplier on enclosed
-conduit subdomains, C10 plain convection, C12 initial data by interpolation,
+conduit subdomains (only with the pressure_art = "free" flag; default C4 fixes delta = 0 on the
+artificial faces), C10 plain convection, C12 initial data by interpolation,
 C13 loads M I_h q, C14 typo fixes, C18 t_{n+1} = (n+1) dt.
 """
 from __future__ import annotations
@@ -122,7 +123,11 @@ class Alg3:
         cls = box.classes()
         n2, n1 = box.node_g.shape[0], box.vert_g.shape[0]
         fixed_v = np.concatenate([cls >= M.ART] * d)
-        fixed = np.concatenate([fixed_v, np.zeros(n1, bool)])
+        # C4: the pressure correction lives in Q_0^h(Omega_j) (compact support): delta = 0 on the
+        # closure of the artificial faces.  Flag pressure_art = "free": delta free there (+ C6 multiplier).
+        p_free_art = self.cfg.get("pressure_art", "zero") == "free"
+        fixed_p = np.zeros(n1, bool) if p_free_art else box.on_artificial(box.vert_g)
+        fixed = np.concatenate([fixed_v, fixed_p])
         gidx = self.box_c.p2_index(box.node_g)
         gidx1 = self.box_c.p1_index(box.vert_g)
         sidx = M.lex_index(np.asarray(sub.index), np.zeros(d, np.int64), np.asarray(self.grid_m))
@@ -135,7 +140,7 @@ class Alg3:
         gp[:, -1] = self.Gp.gamma_g
         PpF = prolongation(self.GpH, gp, self.R, 2) if len(gam) else None
         border = None
-        if sub.enclosed and self.cfg.get("pressure_constraint", "mean_zero") == "mean_zero":
+        if p_free_art and sub.enclosed and self.cfg.get("pressure_constraint", "mean_zero") == "mean_zero":
             border = np.concatenate([np.zeros(d * n2), ops.fem.p1_mass_vector()])
         top = box.node_g[:, -1] == 2 * self.Gc.n[-1]
         return {"sub": sub, "ops": ops, "cls": cls, "fixed": fixed, "gidx": gidx, "gidx1": gidx1, "own": own,
@@ -232,7 +237,8 @@ class Alg3:
         vals_full = np.zeros((d, n2))
         g = pr.velocity(C["X"][dirn], t, C["top"][dirn])
         vals_full[:, dirn] = g - U[:, dirn]  # C5
-        vals = np.concatenate([vals_full[a][fixed[a * n2:(a + 1) * n2]] for a in range(d)])
+        vals = np.concatenate([vals_full[a][fixed[a * n2:(a + 1) * n2]] for a in range(d)]
+                              + [np.zeros(int(fixed[d * n2:].sum()))])
         lu = DirichletLU(K, fixed, C["border"])
         x = lu.solve(b, vals)
         C["last_rel_residual"] = lu.last_rel_residual

@@ -164,6 +164,18 @@ class Box:
             return self.grid.classify(self.node_g)
         return self.grid.classify(self.node_g, self.c0, self.c1)
 
+    def on_artificial(self, g: np.ndarray) -> np.ndarray:
+        """Points g on the closure of the artificial faces dOmega_j \\ dR, ignoring the class precedence
+        (used for the pressure: Q_0^h of P:226 has compact support in Omega_j, reading C4)."""
+        g = np.asarray(g)
+        out = np.zeros(g.shape[:-1], dtype=bool)
+        for a in range(self.d):
+            if self.c0[a] > 0:
+                out |= g[..., a] == 2 * self.c0[a]
+            if self.c1[a] < self.grid.n[a]:
+                out |= g[..., a] == 2 * self.c1[a]
+        return out
+
     def cells(self) -> np.ndarray:
         return lex_points(np.asarray(self.c0), np.asarray(self.c1) - 1)
 
