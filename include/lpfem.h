@@ -1,0 +1,169 @@
+/*
+ * lpfem.h -- C-ABI of the B200 local-parallel two-grid FEM hot path.
+ *
+ * Method: Algorithm 3 of arXiv 2311.05170 ("Local
+ * parallel finite element algorithm"): per backward-Euler step
+ *   Step 1  coarse decoupled marching on T_H          (eqs. pFFully..pcFully)
+ *   Step 3  fine residual corrections on every
+ *           overlapping subdomain Omega_j              (eqs. pFlocalFully,
+ *                                                       pflocalFully, pmlocalFully, uclocalFully)
+ *   Step 4  write-back of the core values D_j
+ * for the transient triple-porosity / Navier-Stokes model with
+ * Taylor-Hood P2-P1 in the conduit and P2 for the three porous pressures
+ * (the paper's r = 1 case).  Readings of the paper where it is
+ * silent are numbered C1..C25 in DESIGN.md; the ones that change an interface
+ * are cited below.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer argument is borrowed for the duration of the call; inputs are
+ *    deep-copied (including lpfem_coeffs.k_mult).  Output buffers are caller-owned.
+ *  - Errors are returned as lpfem_status; no C++ exception crosses the ABI.
+ *    lpfem_last_error() returns a ctx-owned message valid until the next call.
+ *  - One host thread per ctx.  Work is enqueued on lpfem_dist.cuda_stream (NULL =
+ *    the legacy default stream).  lpfem_create/step/get_fields/destroy are
+ *    collective over lpfem_dist.world ranks (one process per GPU).
+ *  - Field layout: global lexicographic order, x fastest.  P2 fields live on the
+ *    (2N_0+1)x(2N_1+1)[x(2N_2+1)] half-grid of their region (porous or conduit),
+ *    P1 (conduit pressure) on the (N_0+1)x... vertices; the velocity is d
+ *    consecutive component arrays (SoA).  Coordinates of half-grid point g are
+ *    lo + g * ((hi - lo) / (2 N)) per axis (C21).
+ *  - Arithmetic: fp64 throughout.
+ */
+#ifndef LPFEM_H
+#define LPFEM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lpfem_ctx lpfem_ctx; /* opaque; owns all device memory */
+
+typedef enum {
+  LPFEM_OK = 0,
+  LPFEM_EINVAL = 1,     /* bad pointer, size or parameter                                  */
+  LPFEM_ENOTDIV = 2,    /* 1/h, 1/H or H/h not integral (relative tolerance 1e-12)            */
+  LPFEM_EMISALIGN = 3,  /* subdomain grid does not divide the fine mesh / overlap not on h   */
+  LPFEM_ENOCONV = 4,    /* Krylov or coarse Picard did not converge; the step is not committed */
+  LPFEM_ECUDA = 5,      /* CUDA runtime error (message in lpfem_last_error)                */
+  LPFEM_ENCCL = 6,      /* NCCL error (multi-GPU only)                                       */
+  LPFEM_ENOMEM = 7,     /* device allocation failed                                          */
+  LPFEM_ESTATE = 8      /* call out of order                                                 */
+} lpfem_status;
+
+enum { LPFEM_PROB_MMS = 0,       /* 2D: paper Ex1; 3D: Ex2 reflected z->1-z (C17) */
+       LPFEM_PROB_INJECTION = 1, /* zero forcing, parabolic inflow on the conduit top face, no-slip sides (C16) */
+       LPFEM_PROB_CONSTANT = 2,  /* p_i = c, u = 0, p = c/rho: an exact discrete steady state (invariant test)  */
+       LPFEM_PROB_MMS_STEADY = 3 /* the MMS frozen at t = 0 (convergence tests)                                 */ };
+enum { LPFEM_LAG_COMPOSITE = 0, /* e~^n from the written-back composite (mode B, default, C2) */
+       LPFEM_LAG_SUBDOMAIN = 1  /* e~^n = the subdomain's own previous correction (mode A, C2) */ };
+
+/* Geometry: two axis-aligned boxes sharing the full face Gamma normal to the last axis;
+ * the conduit lies on the high side (BASELINE configs). */
+typedef struct {
+  int dim; /* 2 or 3 */
+  double porous_lo[3], porous_hi[3], conduit_lo[3], conduit_hi[3];
+} lpfem_geometry;
+
+/* Coefficients.  Arrays are indexed 0 = matrix m, 1 = microfracture f, 2 = macrofracture F. */
+typedef struct {
+  double phi[3], C[3], k[3];
+  double sigma, sigma_star, mu_tilde, nu, rho, alpha, eta;
+  const double* k_mult; /* NULL, or one multiplier per porous COARSE cell (lexicographic, x fastest),
+                           applied to k[0..2] and to k_F on Gamma (C15).  Deep-copied. */
+} lpfem_coeffs;
+
+typedef struct {
+  int problem;        /* LPFEM_PROB_* */
+  double inflow_peak; /* injection: peak inflow speed (1.0) */
+  double const_value; /* constant problem: c */
+} lpfem_data;
+
+typedef struct {
+  int lag_mode;         /* LPFEM_LAG_* */
+  double krylov_rtol;   /* ||b - A x||_2 <= rtol ||b||_2 on every correction system (C19): 1e-12 */
+  int max_iter;         /* per solve, counted in Krylov iterations: e.g. 20000 */
+  int gmres_restart;    /* m of GMRES(m): 30 */
+  double picard_rtol;   /* coarse NS: ||du||_2 <= rtol ||u||_2 (C11): 1e-13 */
+  int picard_max;       /* 50 */
+} lpfem_opts;
+
+typedef struct {
+  int rank, world, device;
+  unsigned char nccl_id[128]; /* from lpfem_nccl_unique_id on rank 0, broadcast by the caller */
+  void* cuda_stream;          /* cudaStream_t or NULL */
+} lpfem_dist;
+
+typedef struct {
+  long long steps;                 /* committed steps */
+  long long fine_iters[2];         /* cumulative Krylov iterations: [porous PCG (sum over systems), conduit GMRES] */
+  long long fine_max_iters[2];     /* max over systems in the last step */
+  long long coarse_iters[2];       /* cumulative coarse iterations: [PCG, GMRES] */
+  long long picard_iters;          /* cumulative coarse Picard iterations */
+  double max_rel_residual[2];      /* last step, max over systems: [porous, conduit] */
+  double t_coarse_ms, t_fine_ms;   /* cumulative device time of the coarse stage and of the fine stage */
+  long long n_systems[2];          /* local systems on this rank: [porous (3 per subdomain), conduit] */
+  long long n_rows[2], nnz[2];     /* local batched sizes: [porous family (per field), conduit family] */
+  long long fine_dofs;             /* D of the metric: 3(2N+1)^d + d(2N+1)^d + (N+1)^d */
+  long long kernel_launches;       /* cumulative launches of this library's kernels */
+  double t_krylov_ms[2];           /* cumulative device time of the fine Krylov launches [PCG, GMRES] (CUDA events) */
+  double bytes_krylov[2];          /* cumulative algorithmic bytes of those launches ("Roofline") */
+  long long krylov_launches[2];    /* number of fine Krylov launches */
+} lpfem_stats;
+
+/* NCCL unique id for a multi-GPU ctx (rank 0 only; world > 1). */
+lpfem_status lpfem_nccl_unique_id(unsigned char out[128]);
+
+/* Build meshes, subdomains (Algorithm 3 Step 2), patterns and the constant
+ * operators; interpolate the initial state (C12).  H, h, overlap are lengths; 1/h, 1/H, H/h and
+ * overlap/h must be integers and subdomain_grid[a] must divide the fine cells per axis of each
+ * region (the grid applies per region, C8).  Collective. */
+lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs, const lpfem_data* data,
+                          double H, double h, double overlap, const int subdomain_grid[3],
+                          const lpfem_opts* opts, const lpfem_dist* dist, lpfem_ctx** out);
+
+/* One step t_n -> t_{n+1} = (n+1) dt (C18): coarse step, fine corrections on
+ * every local subdomain, write-back and halo exchange.  A change
+ * of dt re-assembles the porous operators.  On LPFEM_ENOCONV the state stays at t_n.  Collective. */
+lpfem_status lpfem_step(lpfem_ctx* ctx, double dt);
+
+/* Node counts of the global fine fields: [porous, conduit]. */
+lpfem_status lpfem_get_sizes(const lpfem_ctx* ctx, long long n_nodes_p2[2], long long n_nodes_p1[2]);
+
+/* Copy the composite fine fields at t_n: pF, pf, pm (n_p2[0] each), u (dim * n_p2[1], SoA), p (n_p1[1]).
+ * on_device = 1: the pointers are device pointers on this ctx's GPU; 0: host pointers.  The
+ * owned values of all ranks are gathered on `root` (other ranks may pass NULL).  Collective. */
+lpfem_status lpfem_get_fields(lpfem_ctx* ctx, double* pF, double* pf, double* pm, double* u, double* p,
+                              int on_device, int root);
+
+/* Copy the coarse state at t_n (same layout on the coarse mesh). */
+lpfem_status lpfem_get_coarse_fields(lpfem_ctx* ctx, double* pF, double* pf, double* pm, double* u, double* p);
+
+/* Mesh export for the bit-exact index check (C21, C22).  which = 2*level + region, level 0 coarse /
+ * 1 fine, region 0 porous / 1 conduit.  coords: (n_p2, dim) half-grid node coordinates; cells:
+ * (n_simplices, (dim+1)(dim+2)/2) P2 node indices per simplex (vertices in Kuhn order, then edge
+ * midpoints); any pointer may be NULL.  n_out[0] = n_p2, n_out[1] = n_simplices. */
+lpfem_status lpfem_get_mesh(const lpfem_ctx* ctx, int which, double* coords, int* cells, long long n_out[2]);
+
+/* Subdomain layout of this rank: for each local system k (porous subdomains first, then conduit):
+ * region, lexicographic position, core cells [c0, c1) and extended box cells [e0, e1) per axis.
+ * Arrays hold n*3 ints each; n_out = number of local subdomains. */
+lpfem_status lpfem_get_layout(const lpfem_ctx* ctx, int* region, int* pos, int* core0, int* core1, int* box0,
+                              int* box1, int* n_out);
+
+lpfem_status lpfem_get_stats(const lpfem_ctx* ctx, lpfem_stats* out);
+
+/* Dump the last fine correction system of one local subdomain (debug / parity of a single solve):
+ * family 0 porous (field 0 m, 1 f, 2 F), 1 conduit.  Writes nrows and nnz; if rowptr/col/val/rhs/x
+ * are non-NULL they receive the CSR (rowptr nrows+1 int64, col nnz int32 local, val nnz), the RHS and
+ * the solution.  Host pointers. */
+lpfem_status lpfem_get_system(lpfem_ctx* ctx, int family, int local_index, int field, long long* nrows,
+                              long long* nnz, long long* rowptr, int* col, double* val, double* rhs, double* x);
+
+const char* lpfem_last_error(const lpfem_ctx* ctx);
+const char* lpfem_status_string(lpfem_status s);
+void lpfem_destroy(lpfem_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LPFEM_H */

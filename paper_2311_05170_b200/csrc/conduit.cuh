@@ -1,0 +1,392 @@
+// conduit.cuh -- Taylor-Hood P2-P1 conduit operators (row-gather, atomic-free).
+//
+// Fine correction (Algorithm 3 Step 3(2), eq. uclocalFully), full-field form with
+// U = P u_cH^{n+1} and u = U + e, p = P p_H^{n+1} + delta:
+//   (eta/dt)(u - u~^n, v) + 2 nu eta (D u, D v) + (eta nu alpha/sqrt(k_F)) <P_tau u, P_tau v>_Gamma
+//   + eta((u.grad)U, v) + eta((U.grad)u, v) - eta((U.grad)U, v) - eta(p, div v)
+//   = eta(f, v) - (eta/rho)<P p_FH^n, v.n_c>_Gamma - (eta nu alpha sqrt(k_F)/mu)<grad_tau P p_FH^n, P_tau v>_Gamma,
+//   eta(q, div u) = 0,
+// Coarse step (eq. pcFully) by Picard: the same operator without the reaction term
+// eta((u.grad)U, v) and without -eta((U.grad)U, v), wind W = previous iterate (C11).
+// Signs: n_c = -e_last on Gamma; friction coefficient eta nu alpha sqrt(d)/sqrt(tr Pi) with
+// Pi = k_F I; tangential load coefficient eta nu alpha sqrt(k_F)/mu.
+#pragma once
+#include "assembly.cuh"
+
+namespace lp {
+
+struct ConduitCoefs {
+  double eta, nu, alpha, rho, mu, kF, dt;
+  double schur_w;  // pressure scaling numerator: nu + h^2/(c dt) (preconditioner only)
+};
+
+template <int D>
+__device__ __forceinline__ double gamma_mult(const double* __restrict__ kmult, const Level& L, const SysDesc& S,
+                                             const int c[3], const int nHp[3]) {
+  // k_F multiplier of the porous coarse cell under a Gamma facet at tangential box cell c (C15)
+  if (!kmult) return 1.0;
+  int cc[3];
+  for (int a = 0; a < D - 1; ++a) cc[a] = (S.c0[a] + c[a]) / L.G.R;
+  cc[D - 1] = nHp[D - 1] - 1;
+  return kmult[lex<D>(cc, nHp)];
+}
+
+// length of the comp-0 block of a velocity row (first column >= n2)
+__device__ __forceinline__ long long block_len(const int* __restrict__ col, long long rb, long long re, int n2) {
+  return find_slot(col, rb, re, n2) - rb;
+}
+
+// constant part, unscaled: (eta/dt) M + 2 nu eta D:D + friction_Gamma; -eta(p, div v); eta(q, div u)
+template <int D>
+__global__ void k_conduit_const(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc,
+                                const double* __restrict__ kmult, int nHp0, int nHp1, int nHp2,
+                                const RefT<D>* __restrict__ ref, const long long* __restrict__ rowptr,
+                                const int* __restrict__ col, double* __restrict__ aconst) {
+  const SysDesc S = sys[blockIdx.y];
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= S.nrows) return;
+  constexpr int N = n2_of(D);
+  const int nHp[3] = {nHp0, nHp1, nHp2};
+  const long long rb = rowptr[S.row_off + r], re = rowptr[S.row_off + r + 1];
+  for (long long q = rb; q < re; ++q) aconst[q] = 0.0;
+  const double vol = kuhn_volume<D>(L.G.hc);
+  const int shp1[3] = {S.nc[0] + 1, S.nc[1] + 1, S.nc[2] + 1};
+  int l[3] = {0, 0, 0};
+  if (r < D * S.n2) {
+    const int a = r / S.n2;
+    unlex<D>(r % S.n2, S.np, l);
+    const long long Ln = block_len(col, rb, re, S.n2);
+    for_simplices_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
+      double G[D + 1][D];
+      kuhn_grad<D>(c_kt[D].perm[t], L.G.hc, G);
+      for (int j = 0; j < N; ++j) {
+        int v[3];
+        for (int e = 0; e < D; ++e) v[e] = 2 * c[e] + c_kt[D].off[t][j][e];
+        const int cj = (int)lex<D>(v, S.np);
+        const long long p0 = find_slot(col, rb, rb + Ln, cj);
+        // S_xy = int d_x phi_i d_y phi_j
+        double Sxy[D][D];
+        for (int x = 0; x < D; ++x)
+          for (int y = 0; y < D; ++y) {
+            double s = 0.0;
+            for (int k = 0; k <= D; ++k)
+              for (int m = 0; m <= D; ++m) s += ref->G22[i][k][j][m] * G[k][x] * G[m][y];
+            Sxy[x][y] = vol * s;
+          }
+        double lap = 0.0;
+        for (int x = 0; x < D; ++x) lap += Sxy[x][x];
+        const double nue = cc.nu * cc.eta;
+        for (int b = 0; b < D; ++b) {
+          double v_ab = nue * ((a == b ? lap : 0.0) + Sxy[b][a]);
+          if (a == b) v_ab += (cc.eta / cc.dt) * vol * ref->M22[i][j];
+          aconst[p0 + b * Ln] += v_ab;
+        }
+      }
+      // pressure columns: -eta int psi_m d_a phi_i
+      for (int m = 0; m <= D; ++m) {
+        int v[3];
+        for (int e = 0; e < D; ++e) v[e] = (2 * c[e] + c_kt[D].off[t][m][e]) >> 1;
+        const int key = D * S.n2 + (int)lex<D>(v, shp1);
+        double s = 0.0;
+        for (int k = 0; k <= D; ++k) s += ref->D12[m][i][k] * G[k][a];
+        aconst[find_slot(col, rb + D * Ln, re, key)] += -cc.eta * vol * s;
+      }
+    });
+    // Gamma friction on tangential components
+    if (a < D - 1 && S.has_gamma && 2 * S.c0[D - 1] + l[D - 1] == L.G.gamma_g) {
+      double hf[3] = {L.G.hc[0], L.G.hc[1], 0};
+      const double fvol = kuhn_volume<D - 1>(hf);
+      for_facets_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
+        const double kF = cc.kF * gamma_mult<D>(kmult, L, S, c, nHp);
+        const double fric = cc.eta * cc.nu * cc.alpha / sqrt(kF);
+        for (int j = 0; j < n2_of(D - 1); ++j) {
+          int v[3] = {0, 0, 0};
+          for (int e = 0; e < D - 1; ++e) v[e] = 2 * c[e] + c_kt[D - 1].off[t][j][e];
+          v[D - 1] = l[D - 1];
+          const int cj = (int)lex<D>(v, S.np);
+          aconst[find_slot(col, rb, rb + Ln, cj) + a * Ln] += fric * fvol * ref->MF[i][j];
+        }
+      });
+    }
+  } else {
+    // continuity row of vertex k: eta int psi_k d_b phi_j
+    unlex<D>(r - D * S.n2, shp1, l);
+    for (int e = 0; e < D; ++e) l[e] *= 2;
+    const long long Ln = (re - rb) / D;
+    for_simplices_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
+      double G[D + 1][D];
+      kuhn_grad<D>(c_kt[D].perm[t], L.G.hc, G);
+      for (int j = 0; j < N; ++j) {
+        int v[3];
+        for (int e = 0; e < D; ++e) v[e] = 2 * c[e] + c_kt[D].off[t][j][e];
+        const int cj = (int)lex<D>(v, S.np);
+        const long long p0 = find_slot(col, rb, rb + Ln, cj);
+        for (int b = 0; b < D; ++b) {
+          double s = 0.0;
+          for (int k = 0; k <= D; ++k) s += ref->D12[i][j][k] * G[k][b];
+          aconst[p0 + b * Ln] += cc.eta * vol * s;
+        }
+      }
+    });
+  }
+}
+
+// right preconditioner (diagonal): velocity 1/diag(A_const); pressure schur_w/(eta int psi_k);
+// zero on fixed rows (velocity dir/art nodes, pressure vertices on artificial faces, C4).
+template <int D>
+__global__ void k_conduit_scale(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc,
+                                const long long* __restrict__ rowptr, const int* __restrict__ col,
+                                const double* __restrict__ aconst, double* __restrict__ s) {
+  const SysDesc S = sys[blockIdx.y];
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= S.nrows) return;
+  const long long rb = rowptr[S.row_off + r], re = rowptr[S.row_off + r + 1];
+  int l[3] = {0, 0, 0};
+  double v;
+  if (r < D * S.n2) {
+    unlex<D>(r % S.n2, S.np, l);
+    const bool fixed = node_class<D>(L.G, S, l) >= CL_ART;
+    v = fixed ? 0.0 : 1.0 / aconst[find_slot(col, rb, re, r)];
+  } else {
+    const int shp1[3] = {S.nc[0] + 1, S.nc[1] + 1, S.nc[2] + 1};
+    unlex<D>(r - D * S.n2, shp1, l);
+    for (int e = 0; e < D; ++e) l[e] *= 2;
+    double mk = 0.0;
+    const double vol = kuhn_volume<D>(L.G.hc);
+    for_simplices_at<D>(l, S.nc, [&](const int*, int, int) { mk += vol / (D + 1); });
+    v = vertex_on_art<D>(S, l) ? 0.0 : cc.schur_w / (cc.eta * mk);
+  }
+  s[S.row_off + r] = v;
+}
+
+// per-step preparation (one thread per P2 node or P1 vertex)
+struct ConduitPrepArgs {
+  const double* cu_new;   // coarse conduit velocity (D comps, coarse P2 layout) at n+1 (fine) / Picard iterate (coarse)
+  const double* cp_new;   // coarse conduit pressure at n+1 (fine) / Picard iterate (coarse)
+  const double* cu_old;   // coarse conduit velocity at n
+  const double* cpF_old;  // coarse porous p_F at n
+  const double* comp_u;   // global fine composite velocity (mode B)
+  const double* ecorr;    // mode A corrections (row space) or NULL
+  int nHc[3], nHp[3];
+  int R;
+  int np_glob[3];         // P2 nodes per axis of the level's conduit region
+  long long n2_glob;      // P2 nodes of the level's conduit region (component stride)
+  int porous_gamma_g;     // half-grid index of Gamma in the porous region at the coarse level x R
+  int mode;               // 0 fine composite (B), 1 fine subdomain (A), 2 coarse Picard
+  double t;
+};
+
+template <int D>
+__global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbData pd, Coef co, ConduitPrepArgs A,
+                               double* __restrict__ base, double* __restrict__ z, double* __restrict__ W,
+                               double* __restrict__ lag, double* __restrict__ f, double* __restrict__ pfg) {
+  const SysDesc S = sys[blockIdx.y];
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= S.n2 + S.n1) return;
+  const long long o = S.row_off;
+  int l[3] = {0, 0, 0}, g[3] = {0, 0, 0};
+  double x[3] = {0, 0, 0};
+  if (r < S.n2) {
+    unlex<D>(r, S.np, l);
+    for (int a = 0; a < D; ++a) {
+      g[a] = 2 * S.c0[a] + l[a];
+      x[a] = L.G.lo[a] + g[a] * L.G.hg[a];
+    }
+    const int cls = node_class<D>(L.G, S, l);
+    const bool top = g[D - 1] == 2 * L.G.n[D - 1];
+    double gv[3], fv[3];
+    velocity_values<D>(pd, x, A.t, top, gv);
+    velocity_forcing<D>(pd, co, x, A.t, fv);
+    const int shpH[3] = {2 * A.nHc[0] + 1, 2 * A.nHc[1] + 1, 2 * A.nHc[2] + 1};
+    const long long n2H = (long long)shpH[0] * shpH[1] * (D > 2 ? shpH[2] : 1);
+    for (int a = 0; a < D; ++a) {
+      const long long k = o + a * S.n2 + r;
+      double b, lg;
+      if (A.mode == 2) {
+        const long long gi = lex<D>(g, A.np_glob);
+        b = A.cu_new[a * A.n2_glob + gi];
+        lg = A.cu_old[a * A.n2_glob + gi];
+      } else {
+        b = prolong_p2<D>(A.cu_new + a * n2H, A.nHc, A.R, g);
+        if (A.mode == 0) lg = A.comp_u[a * A.n2_glob + lex<D>(g, A.np_glob)];
+        else lg = prolong_p2<D>(A.cu_old + a * n2H, A.nHc, A.R, g) + A.ecorr[k];
+      }
+      base[k] = b;
+      W[k] = b;
+      z[k] = cls == CL_DIR ? gv[a] : b;
+      lag[k] = lg;
+      f[k] = fv[a];
+    }
+    double pf = 0.0;
+    if (g[D - 1] == L.G.gamma_g) {
+      int gp[3] = {g[0], g[1], g[2]};
+      gp[D - 1] = A.porous_gamma_g;
+      pf = prolong_p2<D>(A.cpF_old, A.nHp, A.R, gp);
+    }
+    pfg[o + r] = pf;
+  } else {
+    const int k1 = r - S.n2;
+    const int shp1[3] = {S.nc[0] + 1, S.nc[1] + 1, S.nc[2] + 1};
+    unlex<D>(k1, shp1, l);
+    for (int a = 0; a < D; ++a) g[a] = 2 * (S.c0[a] + l[a]);
+    double b;
+    if (A.mode == 2) {
+      int v[3];
+      for (int a = 0; a < D; ++a) v[a] = g[a] / 2;
+      const int shpg1[3] = {(A.np_glob[0] + 1) / 2, (A.np_glob[1] + 1) / 2, (A.np_glob[2] + 1) / 2};
+      b = A.cp_new[lex<D>(v, shpg1)];
+    } else {
+      b = prolong_p1<D>(A.cp_new, A.nHc, A.R, g);
+    }
+    const long long k = o + D * S.n2 + k1;
+    base[k] = b;
+    z[k] = b;
+  }
+}
+
+// Per-step operator: A' = mask * (A_const + eta N(W) [+ eta R(U)]) * diag(s) and right-hand side
+// rhs = mask * (b_load - A z), b_load = eta M f + (eta/dt) M u~^n [+ eta N(U) U] + Gamma loads.
+template <int D>
+__global__ void k_conduit_step(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int newton,
+                               const double* __restrict__ kmult, int nHp0, int nHp1, int nHp2,
+                               const RefT<D>* __restrict__ ref, const long long* __restrict__ rowptr,
+                               const int* __restrict__ col, const double* __restrict__ aconst,
+                               const double* __restrict__ s, const double* __restrict__ z,
+                               const double* __restrict__ W, const double* __restrict__ lag,
+                               const double* __restrict__ f, const double* __restrict__ pfg,
+                               double* __restrict__ aout, double* __restrict__ rhs) {
+  const SysDesc S = sys[blockIdx.y];
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= S.nrows) return;
+  constexpr int N = n2_of(D);
+  const int nHp[3] = {nHp0, nHp1, nHp2};
+  const long long o = S.row_off;
+  const long long rb = rowptr[o + r], re = rowptr[o + r + 1];
+  const double* zs = z + o;
+  const double* ss = s + o;
+  for (long long q = rb; q < re; ++q) aout[q] = aconst[q];
+  double b = 0.0;
+  if (r < D * S.n2) {
+    const int a = r / S.n2;
+    int l[3] = {0, 0, 0};
+    unlex<D>(r % S.n2, S.np, l);
+    const long long Ln = block_len(col, rb, re, S.n2);
+    const double vol = kuhn_volume<D>(L.G.hc);
+    const double* Ws = W + o;
+    const double* Ls = lag + o + a * S.n2;
+    const double* Fs = f + o + a * S.n2;
+    for_simplices_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
+      double G[D + 1][D];
+      kuhn_grad<D>(c_kt[D].perm[t], L.G.hc, G);
+      int idx[N];
+      double We[D][N];
+      for (int j = 0; j < N; ++j) {
+        int v[3];
+        for (int e = 0; e < D; ++e) v[e] = 2 * c[e] + c_kt[D].off[t][j][e];
+        idx[j] = (int)lex<D>(v, S.np);
+        for (int e = 0; e < D; ++e) We[e][j] = Ws[e * S.n2 + idx[j]];
+      }
+      // w_l(m) = W(m) . grad lam_l
+      double wl[D + 1][N];
+      for (int k = 0; k <= D; ++k)
+        for (int m = 0; m < N; ++m) {
+          double s2 = 0.0;
+          for (int e = 0; e < D; ++e) s2 += We[e][m] * G[k][e];
+          wl[k][m] = s2;
+        }
+      const double ev = cc.eta * vol;
+      for (int j = 0; j < N; ++j) {
+        const long long p0 = find_slot(col, rb, rb + Ln, idx[j]);
+        // convection eta int phi_i (W.grad phi_j)
+        double cv = 0.0;
+        for (int k = 0; k <= D; ++k)
+          for (int m = 0; m < N; ++m) cv += ref->C3[i][m][j][k] * wl[k][m];
+        cv *= ev;
+        aout[p0 + a * Ln] += cv;
+        b += vol * ref->M22[i][j] * (cc.eta * Fs[idx[j]] + (cc.eta / cc.dt) * Ls[idx[j]]);
+        if (newton) {
+          b += cv * We[a][j];  // eta ((U.grad)U, v)
+          // reaction eta int phi_i phi_j d_b U_a = eta sum_m U_a(m) sum_k C3[i][j][m][k] G[k][b]
+          for (int bb = 0; bb < D; ++bb) {
+            double rv = 0.0;
+            for (int m = 0; m < N; ++m) {
+              double t2 = 0.0;
+              for (int k = 0; k <= D; ++k) t2 += ref->C3[i][j][m][k] * G[k][bb];
+              rv += We[a][m] * t2;
+            }
+            aout[p0 + bb * Ln] += ev * rv;
+          }
+        }
+      }
+    });
+    if (S.has_gamma && 2 * S.c0[D - 1] + l[D - 1] == L.G.gamma_g) {
+      double hf[3] = {L.G.hc[0], L.G.hc[1], 0};
+      const double fvol = kuhn_volume<D - 1>(hf);
+      const double* P = pfg + o;
+      for_facets_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
+        const double kF = cc.kF * gamma_mult<D>(kmult, L, S, c, nHp);
+        double Gt[D][D - 1];
+        double hf2[3] = {L.G.hc[0], L.G.hc[1], 0};
+        kuhn_grad<D - 1>(c_kt[D - 1].perm[t], hf2, Gt);
+        for (int j = 0; j < n2_of(D - 1); ++j) {
+          int v[3] = {0, 0, 0};
+          for (int e = 0; e < D - 1; ++e) v[e] = 2 * c[e] + c_kt[D - 1].off[t][j][e];
+          v[D - 1] = l[D - 1];
+          const double pj = P[lex<D>(v, S.np)];
+          if (a == D - 1) {
+            b += (cc.eta / cc.rho) * fvol * ref->MF[i][j] * pj;  // -(eta/rho)<p_F, v.n_c>, n_c = -e_last
+          } else {
+            const double ct = cc.eta * cc.nu * cc.alpha * sqrt(kF) / cc.mu;
+            double tg = 0.0;
+            for (int k = 0; k < D; ++k) tg += ref->TF[i][j][k] * Gt[k][a];
+            b -= ct * fvol * tg * pj;  // -(eta nu alpha sqrt(k_F)/mu)<grad_tau p_F, P_tau v>
+          }
+        }
+      });
+    }
+  }
+  for (long long q = rb; q < re; ++q) b -= aout[q] * zs[col[q]];
+  const bool fixed = ss[r] == 0.0;
+  for (long long q = rb; q < re; ++q) aout[q] = fixed ? 0.0 : aout[q] * ss[col[q]];
+  rhs[o + r] = fixed ? 0.0 : b;
+}
+
+// write-back of the conduit solution: u = z + s y (velocity), p = z + s y (pressure) on owned nodes.
+template <int D>
+__global__ void k_conduit_writeback(const SysDesc* __restrict__ sys, Level L, const double* __restrict__ z,
+                                    const double* __restrict__ y, const double* __restrict__ s,
+                                    const double* __restrict__ base, double* __restrict__ ecorr,
+                                    double* __restrict__ out_u, double* __restrict__ out_p, int np0, int np1,
+                                    int np2, long long n2_glob) {
+  const SysDesc S = sys[blockIdx.y];
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= S.n2 + S.n1) return;
+  const long long o = S.row_off;
+  const int npg[3] = {np0, np1, np2};
+  int l[3] = {0, 0, 0}, g[3] = {0, 0, 0};
+  if (r < S.n2) {
+    unlex<D>(r, S.np, l);
+    for (int a = 0; a < D; ++a) g[a] = 2 * S.c0[a] + l[a];
+    const bool own = owns<D>(L, S, g);
+    const long long gi = lex<D>(g, npg);
+    for (int a = 0; a < D; ++a) {
+      const long long k = o + a * S.n2 + r;
+      const double full = z[k] + s[k] * y[k];
+      if (own) out_u[a * n2_glob + gi] = full;
+      if (ecorr) ecorr[k] = full - base[k];
+    }
+  } else {
+    const int k1 = r - S.n2;
+    const int shp1[3] = {S.nc[0] + 1, S.nc[1] + 1, S.nc[2] + 1};
+    unlex<D>(k1, shp1, l);
+    for (int a = 0; a < D; ++a) g[a] = 2 * (S.c0[a] + l[a]);
+    if (!owns<D>(L, S, g)) return;
+    int v[3];
+    for (int a = 0; a < D; ++a) v[a] = g[a] / 2;
+    const int shpg1[3] = {(npg[0] + 1) / 2, (npg[1] + 1) / 2, (npg[2] + 1) / 2};
+    const long long k = o + D * S.n2 + k1;
+    out_p[lex<D>(v, shpg1)] = z[k] + s[k] * y[k];
+  }
+}
+
+}  // namespace lp

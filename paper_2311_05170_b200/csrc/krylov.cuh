@@ -1,0 +1,392 @@
+// krylov.cuh -- batched Krylov solvers for the local correction systems.
+//
+// Design (B200): one thread-block cluster owns one linear system for the whole solve.  Every
+// iteration runs inside a single kernel launch: the SpMV, the vector updates and the dot products
+// are passes over the cluster's rows, and each reduction is a fixed-order warp-shuffle / shared
+// memory / DSMEM sum, so results are deterministic and there is no host round trip.  Systems are
+// independent (every subdomain correction reads only coarse data and its own lagged
+// state), so the grid is simply (systems x cluster size).
+//
+//  * k_cg     conjugate gradients on the symmetrically Jacobi-scaled SPD porous systems
+//             A~ = D^-1/2 A D^-1/2 (fixed rows/columns zero).  The stopping test uses the
+//             unscaled residual ||b - A x||_2 = ||D^1/2 r~||_2 <= rtol ||b||_2 (C19) via the weights
+//             w = diag(A); converged solves are re-checked with the true residual.
+//  * k_gmres  restarted GMRES(M) with classical Gram-Schmidt and one re-orthogonalisation (CGS2),
+//             Givens rotations, on the right-scaled saddle systems A' = mask A diag(s) (block-diagonal
+//             preconditioner: velocity Jacobi, pressure mass Schur approximation).  Right
+//             preconditioning keeps the residual of the original system, so the test
+//             ||b - A x||_2 <= rtol ||b||_2 (C19) is exact; every restart recomputes it.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace lp {
+namespace cgx = cooperative_groups;
+
+struct KSys {
+  long long row_off;   // vectors: first row of this system in the family's vector row space
+  long long prow_off;  // pattern: first row of this system in rowptr
+  long long val_off;   // values: offset added to rowptr positions
+  int nrows;
+  int pad;
+};
+
+struct KStat {
+  int iters;
+  int converged;
+  double relres;  // final ||b - A x|| / ||b|| (true residual)
+  long long vsum; // GMRES: sum over iterations of (j + 1), the basis vectors read per Gram-Schmidt pass
+  long long spmv; // SpMV passes (iterations + residual checks)
+};
+
+struct KArgs {
+  const KSys* sys;
+  const long long* rowptr;
+  const int* col;
+  const double* val;
+  const double* b;
+  const double* w;   // CG: residual-norm weights (diag of the unscaled operator); unused by GMRES
+  double* x;
+  double* r;
+  double* p;         // CG: search direction; GMRES: W work vector
+  double* q;         // CG: A p
+  double* V;         // GMRES basis, (M+1) x rows_total
+  long long rows_total;
+  double rtol;
+  int maxit;
+  KStat* stat;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NT, int NV>
+struct RedSmem {
+  double red[NT / 32][NV];
+  double cred[2][NV];
+  double fin[NV];
+};
+
+// Sum over the cluster of per-warp partials already stored in S.red[warp][0..n); returns via S.fin.
+template <int NT, int NV>
+__device__ __forceinline__ void cluster_sum(RedSmem<NT, NV>& S, int n, int& par) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  __syncthreads();
+  const int tid = threadIdx.x;
+  if (tid < n) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += S.red[w][tid];
+    S.cred[par][tid] = s;
+  }
+  cl.sync();
+  if (tid < n) {
+    double s = 0.0;
+    const int nb = (int)cl.num_blocks();
+    for (int k = 0; k < nb; ++k) s += cl.map_shared_rank(&S.cred[par][0], k)[tid];
+    S.fin[tid] = s;
+  }
+  __syncthreads();
+  par ^= 1;
+}
+
+template <int NT, int NV>
+__device__ __forceinline__ void put_partial(RedSmem<NT, NV>& S, int k, double v) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5][k] = v;
+}
+
+// y[i] = sum_q val[q] x[col[q]] for rows [r0, r1), TPR lanes per row; returns nothing, writes y
+template <int NT, int TPR>
+__device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, const int* __restrict__ col,
+                                          const double* __restrict__ val, const double* __restrict__ x,
+                                          double* __restrict__ y, int r0, int r1) {
+  const int lane = threadIdx.x % TPR;
+  const int grp = threadIdx.x / TPR;
+  constexpr int NG = NT / TPR;
+  for (int base = r0; base < r1; base += NG) {
+    const int r = base + grp;
+    double s = 0.0;
+    if (r < r1) {
+      const long long qb = rp[r], qe = rp[r + 1];
+      for (long long q = qb + lane; q < qe; q += TPR) s += val[q] * x[col[q]];
+    }
+#pragma unroll
+    for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
+    if (r < r1 && lane == 0) y[r] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+template <int NT, int TPR>
+__global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const int sid = blockIdx.x / CL;
+  const KSys K = A.sys[sid];
+  const int chunk = (K.nrows + CL - 1) / CL;
+  const int r0 = min(K.nrows, crank * chunk), r1 = min(K.nrows, r0 + chunk);
+  const long long* rp = A.rowptr + K.prow_off;
+  const int* col = A.col;
+  const double* val = A.val + K.val_off;
+  const double* b = A.b + K.row_off;
+  const double* w = A.w + K.row_off;
+  double* x = A.x + K.row_off;
+  double* r = A.r + K.row_off;
+  double* p = A.p + K.row_off;
+  double* q = A.q + K.row_off;
+  __shared__ RedSmem<NT, 2> S;
+  int par = 0;
+  const int tid = threadIdx.x;
+
+  double pw = 0.0, pz = 0.0;
+  for (int i = r0 + tid; i < r1; i += NT) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    p[i] = bi;
+    pw += w[i] * bi * bi;
+    pz += bi * bi;
+  }
+  put_partial(S, 0, pw);
+  put_partial(S, 1, pz);
+  cluster_sum(S, 2, par);
+  const double bnorm = sqrt(S.fin[0]);
+  double rz = S.fin[1];
+  int it = 0, conv = 0, nspmv = 0;
+  double relres = 0.0;
+  if (bnorm == 0.0) {
+    conv = 1;
+  } else {
+    const double tol2 = A.rtol * A.rtol * S.fin[0];
+    int checks = 0;
+    while (true) {
+      cl.sync();  // p complete across the cluster
+      spmv_rows<NT, TPR>(rp, col, val, p, q, r0, r1);
+      __syncthreads();
+      double ppq = 0.0;
+      for (int i = r0 + tid; i < r1; i += NT) ppq += p[i] * q[i];
+      put_partial(S, 0, ppq);
+      cluster_sum(S, 1, par);
+      const double pq = S.fin[0];
+      const double alpha = pq != 0.0 ? rz / pq : 0.0;
+      double prr = 0.0, prz = 0.0;
+      for (int i = r0 + tid; i < r1; i += NT) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        prr += w[i] * ri * ri;
+        prz += ri * ri;
+      }
+      put_partial(S, 0, prr);
+      put_partial(S, 1, prz);
+      cluster_sum(S, 2, par);
+      ++it;
+      const double rrw = S.fin[0], rzn = S.fin[1];
+      if (rrw <= tol2 || it >= A.maxit || pq == 0.0) {
+        // verify with the true residual r = b - A x
+        ++nspmv;
+        cl.sync();
+        spmv_rows<NT, TPR>(rp, col, val, x, q, r0, r1);
+        __syncthreads();
+        double pt = 0.0, pzz = 0.0;
+        for (int i = r0 + tid; i < r1; i += NT) {
+          const double ri = b[i] - q[i];
+          r[i] = ri;
+          p[i] = ri;
+          pt += w[i] * ri * ri;
+          pzz += ri * ri;
+        }
+        put_partial(S, 0, pt);
+        put_partial(S, 1, pzz);
+        cluster_sum(S, 2, par);
+        relres = sqrt(S.fin[0]) / bnorm;
+        if (S.fin[0] <= tol2) {
+          conv = 1;
+          break;
+        }
+        if (it >= A.maxit || ++checks > 20 || pq == 0.0) break;
+        rz = S.fin[1];
+        continue;  // restart from the true residual
+      }
+      const double beta = rzn / rz;
+      rz = rzn;
+      for (int i = r0 + tid; i < r1; i += NT) p[i] = r[i] + beta * p[i];
+    }
+  }
+  if (crank == 0 && tid == 0) {
+    A.stat[sid].iters = it;
+    A.stat[sid].converged = conv;
+    A.stat[sid].relres = relres;
+    A.stat[sid].vsum = 0;
+    A.stat[sid].spmv = it + nspmv;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+template <int NT, int TPR, int M>
+__global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const int sid = blockIdx.x / CL;
+  const KSys K = A.sys[sid];
+  const int chunk = (K.nrows + CL - 1) / CL;
+  const int r0 = min(K.nrows, crank * chunk), r1 = min(K.nrows, r0 + chunk);
+  const long long* rp = A.rowptr + K.prow_off;
+  const int* col = A.col;
+  const double* val = A.val + K.val_off;
+  const double* b = A.b + K.row_off;
+  double* x = A.x + K.row_off;
+  double* r = A.r + K.row_off;
+  double* W = A.p + K.row_off;
+  const long long ld = A.rows_total;
+  double* V = A.V + K.row_off;
+  __shared__ RedSmem<NT, M + 1> S;
+  __shared__ double H[M + 1][M], cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1];
+  int par = 0;
+  const int tid = threadIdx.x;
+
+  double pb = 0.0;
+  for (int i = r0 + tid; i < r1; i += NT) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    pb += bi * bi;
+  }
+  put_partial(S, 0, pb);
+  cluster_sum(S, 1, par);
+  const double bnorm = sqrt(S.fin[0]);
+  double beta = bnorm;
+  const double tol = A.rtol * bnorm;
+  int it = 0, conv = 0, nspmv = 0;
+  long long vsum = 0;
+  if (bnorm == 0.0) conv = 1;
+  while (!conv) {
+    for (int i = r0 + tid; i < r1; i += NT) V[i] = r[i] / beta;
+    if (tid == 0) {
+      gv[0] = beta;
+      for (int k = 1; k <= M; ++k) gv[k] = 0.0;
+    }
+    int jend = 0;
+    for (int j = 0; j < M; ++j) {
+      cl.sync();  // V_j complete
+      spmv_rows<NT, TPR>(rp, col, val, V + j * ld, W, r0, r1);
+      __syncthreads();
+      // CGS pass 1: h = V^T W
+      double acc[M + 1];
+#pragma unroll
+      for (int k = 0; k <= M; ++k) acc[k] = 0.0;
+      for (int i = r0 + tid; i < r1; i += NT) {
+        const double wi = W[i];
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k <= j) acc[k] += V[k * ld + i] * wi;
+      }
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (k <= j) put_partial(S, k, acc[k]);
+      cluster_sum(S, j + 1, par);
+      if (tid <= j) hc[tid] = S.fin[tid];
+      __syncthreads();
+      // pass 2: W -= V h; h2 = V^T W
+#pragma unroll
+      for (int k = 0; k <= M; ++k) acc[k] = 0.0;
+      for (int i = r0 + tid; i < r1; i += NT) {
+        double wi = W[i];
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k <= j) wi -= hc[k] * V[k * ld + i];
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k <= j) acc[k] += V[k * ld + i] * wi;
+        W[i] = wi;
+      }
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (k <= j) put_partial(S, k, acc[k]);
+      cluster_sum(S, j + 1, par);
+      // pass 3: W -= V h2; ||W||
+      double pn = 0.0;
+      for (int i = r0 + tid; i < r1; i += NT) {
+        double wi = W[i];
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k <= j) wi -= S.fin[k] * V[k * ld + i];
+        W[i] = wi;
+        pn += wi * wi;
+      }
+      if (tid <= j) hc[tid] += S.fin[tid];
+      __syncthreads();
+      put_partial(S, 0, pn);
+      cluster_sum(S, 1, par);
+      const double hn = sqrt(S.fin[0]);
+      if (hn > 0.0)
+        for (int i = r0 + tid; i < r1; i += NT) V[(j + 1) * ld + i] = W[i] / hn;
+      if (tid == 0) {
+        for (int k = 0; k <= j; ++k) H[k][j] = hc[k];
+        H[j + 1][j] = hn;
+        for (int k = 0; k < j; ++k) {
+          const double a = H[k][j], c = H[k + 1][j];
+          H[k][j] = cs[k] * a + sn[k] * c;
+          H[k + 1][j] = -sn[k] * a + cs[k] * c;
+        }
+        const double a = H[j][j], c = H[j + 1][j];
+        const double den = hypot(a, c);
+        cs[j] = den > 0.0 ? a / den : 1.0;
+        sn[j] = den > 0.0 ? c / den : 0.0;
+        H[j][j] = den;
+        H[j + 1][j] = 0.0;
+        gv[j + 1] = -sn[j] * gv[j];
+        gv[j] = cs[j] * gv[j];
+      }
+      __syncthreads();
+      ++it;
+      vsum += j + 1;
+      jend = j + 1;
+      if (fabs(gv[j + 1]) <= tol || it >= A.maxit || hn == 0.0) break;
+    }
+    // y = H^-1 g (upper triangular, jend x jend)
+    if (tid == 0) {
+      for (int k = jend - 1; k >= 0; --k) {
+        double s = gv[k];
+        for (int m = k + 1; m < jend; ++m) s -= H[k][m] * yv[m];
+        yv[k] = H[k][k] != 0.0 ? s / H[k][k] : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int i = r0 + tid; i < r1; i += NT) {
+      double s = x[i];
+      for (int k = 0; k < jend; ++k) s += yv[k] * V[k * ld + i];
+      x[i] = s;
+    }
+    cl.sync();
+    ++nspmv;
+    spmv_rows<NT, TPR>(rp, col, val, x, W, r0, r1);
+    __syncthreads();
+    double pr = 0.0;
+    for (int i = r0 + tid; i < r1; i += NT) {
+      const double ri = b[i] - W[i];
+      r[i] = ri;
+      pr += ri * ri;
+    }
+    put_partial(S, 0, pr);
+    cluster_sum(S, 1, par);
+    beta = sqrt(S.fin[0]);
+    if (beta <= tol) conv = 1;
+    if (it >= A.maxit || beta == 0.0) break;
+  }
+  if (crank == 0 && tid == 0) {
+    A.stat[sid].iters = it;
+    A.stat[sid].converged = conv;
+    A.stat[sid].relres = bnorm > 0.0 ? beta / bnorm : 0.0;
+    A.stat[sid].vsum = vsum;
+    A.stat[sid].spmv = it + nspmv;
+  }
+}
+
+}  // namespace lp

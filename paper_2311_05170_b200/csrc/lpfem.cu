@@ -1,0 +1,1249 @@
+// lpfem.cu -- context, setup (stage a0), the per-step driver of Algorithm 3 and the C-ABI.
+//
+// Paper: Algorithm 3.  Step 1 (coarse) runs redundantly on every GPU with
+// the same kernels as the fine stage (one "system" per coarse region); Step 3 solves
+// every local correction as a batch; Step 4 writes core values back.  See DESIGN.md.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/lpfem.h"
+#include "assembly.cuh"
+#include "conduit.cuh"
+#include "krylov.cuh"
+#include "problem.cuh"
+#include "tables.h"
+
+using namespace lp;
+
+namespace {
+
+struct Err : std::runtime_error {
+  lpfem_status code;
+  Err(lpfem_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw Err(LPFEM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +          \
+                                 std::to_string(__LINE__));                                        \
+  } while (0)
+
+thread_local long long tl_launches = 0;  // kernel launches of this library (host thread of the ctx)
+#define CKL()                      \
+  do {                             \
+    CK(cudaGetLastError());        \
+    ++tl_launches;                 \
+  } while (0)
+
+template <class T>
+T* dalloc(size_t n) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) throw Err(LPFEM_ENOMEM, std::string("cudaMalloc ") + std::to_string(n * sizeof(T)) + " B: " + cudaGetErrorString(e));
+  return (T*)p;
+}
+
+constexpr int GM = 30;  // GMRES restart length (compile-time register blocking)
+
+struct Family {
+  int kind = 0;   // 0 porous (scalar P2, 3 fields), 1 conduit (Taylor-Hood saddle)
+  int level = 1;  // 0 coarse, 1 fine
+  std::vector<SysDesc> hs;
+  SysDesc* ds = nullptr;
+  long long rows = 0, nnz = 0;
+  int maxrows = 0, maxitems = 0;
+  long long* rowptr = nullptr;
+  int* col = nullptr;
+  // porous
+  double *val = nullptr, *diag = nullptr, *isq = nullptr, *wn = nullptr;
+  // conduit
+  double *aconst = nullptr, *aout = nullptr, *scale = nullptr;
+  // vectors
+  double *base = nullptr, *z = nullptr, *lag = nullptr, *qf = nullptr, *aux = nullptr, *W = nullptr;
+  double *rhs = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *V = nullptr, *ecorr = nullptr;
+  std::vector<KSys> hk;
+  KSys* dk = nullptr;
+  KStat* dstat = nullptr;
+  std::vector<KStat> hstat;
+  int cluster = 1;
+  std::vector<long long> sys_nnz;        // nnz per Krylov system
+  std::vector<int> sub_region, sub_pos;  // per local subdomain (fine)
+  std::vector<std::array<int, 3>> core0, core1;
+  void free_all() {
+    void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, aconst, aout, scale, base, z, lag, qf, aux, W,
+                    rhs, x, r, p, q, V, ecorr, dk, dstat};
+    for (void* ptr : ptrs)
+      if (ptr) cudaFree(ptr);
+  }
+};
+
+}  // namespace
+
+struct lpfem_ctx {
+  int D = 2;
+  lpfem_geometry geom{};
+  Coef co{};
+  ProbData pd{};
+  lpfem_opts opts{};
+  lpfem_dist dist{};
+  double H = 0, h = 0;
+  int R = 1, ov = 0, m[3] = {1, 1, 1};
+  int nf_p[3] = {1, 1, 1}, nf_c[3] = {1, 1, 1}, nc_p[3] = {1, 1, 1}, nc_c[3] = {1, 1, 1};
+  Level Lp[2], Lc[2];  // [level] porous, conduit
+  Family fam[2][2];    // [level][kind]
+  // coarse state [old/new]
+  double* cst[2][3] = {};
+  double* cu[2] = {};
+  double* cp[2] = {};
+  double *wpic = nullptr, *wpic2 = nullptr, *ppic = nullptr, *ppic2 = nullptr;
+  double* nrm = nullptr;  // 2 doubles
+  // composite fine fields
+  double* comp[3] = {};
+  double* comp_u = nullptr;
+  double* comp_p = nullptr;
+  long long n2p_f = 0, n2c_f = 0, n1c_f = 0, n2p_c = 0, n2c_c = 0, n1c_c = 0;
+  double* kmult = nullptr;
+  std::vector<double> hkmult;
+  void* ref = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[4] = {};
+  cudaEvent_t ek[4] = {};
+  lpfem_stats stats{};
+  std::string err;
+  long long nstep = 0;
+  double cur_dt = -1.0;
+  double schur_c = 1.0;
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------------ host setup
+void upload_tables() {
+  static bool done = false;
+  if (done) return;
+  KuhnTables kt[4];
+  for (int d = 1; d <= 3; ++d) build_kuhn(d, kt[d]);
+  CK(cudaMemcpyToSymbol(c_kt, kt, sizeof(kt)));
+  // neighbour offsets per parity class, from the simplices around an interior reference node
+  static signed char nb[4][8][72][3], nb1[4][8][32][3];
+  static int nbn[4][8], nb1n[4][8];
+  std::memset(nb, 0, sizeof(nb));
+  std::memset(nb1, 0, sizeof(nb1));
+  std::memset(nbn, 0, sizeof(nbn));
+  std::memset(nb1n, 0, sizeof(nb1n));
+  for (int d = 2; d <= 3; ++d) {
+    const KuhnTables& T = kt[d];
+    const int nt = nt_of(d), N = n2_of(d);
+    for (int k = 0; k < (1 << d); ++k) {
+      int l[3] = {0, 0, 0};
+      for (int a = 0; a < d; ++a) l[a] = 8 + ((k >> a) & 1);
+      std::vector<std::array<int, 3>> p2, p1;
+      for (int c2 = 2; c2 <= (d > 2 ? 6 : 2); ++c2)
+        for (int c1 = 2; c1 <= 6; ++c1)
+          for (int c0 = 2; c0 <= 6; ++c0) {
+            int c[3] = {c0, c1, d > 2 ? c2 : 0};
+            bool inside = true;
+            int code = 0, s = 1;
+            for (int a = 0; a < d; ++a, s *= 3) {
+              int o = l[a] - 2 * c[a];
+              inside = inside && o >= 0 && o <= 2;
+              code += o * s;
+            }
+            if (!inside) continue;
+            for (int t = 0; t < nt; ++t) {
+              if (T.lookup[t][code] < 0) continue;
+              for (int j = 0; j < N; ++j) {
+                std::array<int, 3> v = {0, 0, 0};
+                for (int a = 0; a < d; ++a) v[a] = 2 * c[a] + T.off[t][j][a] - l[a];
+                p2.push_back(v);
+                if (j <= d) p1.push_back(v);
+              }
+            }
+          }
+      auto key = [](const std::array<int, 3>& v) { return ((v[2] + 4) * 9 + (v[1] + 4)) * 9 + (v[0] + 4); };
+      auto srt = [&](std::vector<std::array<int, 3>>& vv) {
+        std::sort(vv.begin(), vv.end(), [&](auto& a, auto& b) { return key(a) < key(b); });
+        vv.erase(std::unique(vv.begin(), vv.end()), vv.end());
+      };
+      srt(p2);
+      srt(p1);
+      if (p2.size() > 72 || p1.size() > 32) throw Err(LPFEM_EINVAL, "neighbour table overflow");
+      nbn[d][k] = (int)p2.size();
+      nb1n[d][k] = (int)p1.size();
+      for (size_t i = 0; i < p2.size(); ++i)
+        for (int a = 0; a < 3; ++a) nb[d][k][i][a] = (signed char)p2[i][a];
+      for (size_t i = 0; i < p1.size(); ++i)
+        for (int a = 0; a < 3; ++a) nb1[d][k][i][a] = (signed char)p1[i][a];
+    }
+  }
+  CK(cudaMemcpyToSymbol(c_nb, nb, sizeof(nb)));
+  CK(cudaMemcpyToSymbol(c_nbn, nbn, sizeof(nbn)));
+  CK(cudaMemcpyToSymbol(c_nb1, nb1, sizeof(nb1)));
+  CK(cudaMemcpyToSymbol(c_nb1n, nb1n, sizeof(nb1n)));
+  done = true;
+}
+
+int to_int_checked(double v, lpfem_status code, const char* what) {
+  double r = std::round(v);
+  if (r < 1 || std::fabs(v - r) > 1e-12 * std::max(1.0, std::fabs(v)))
+    throw Err(code, std::string(what) + " is not a positive integer");
+  return (int)r;
+}
+
+LevelGeom make_level(int D, const double* lo, const double* hi, int region, double step, int R) {
+  LevelGeom G{};
+  for (int a = 0; a < 3; ++a) {
+    G.n[a] = 1;
+    G.lo[a] = 0;
+    G.hi[a] = 0;
+    G.hc[a] = 1;
+    G.hg[a] = 1;
+  }
+  for (int a = 0; a < D; ++a) {
+    G.n[a] = to_int_checked((hi[a] - lo[a]) / step, LPFEM_ENOTDIV, "region extent / mesh size");
+    G.lo[a] = lo[a];
+    G.hi[a] = hi[a];
+    G.hc[a] = (hi[a] - lo[a]) / G.n[a];
+    G.hg[a] = (hi[a] - lo[a]) / (2 * G.n[a]);
+  }
+  G.R = R;
+  G.region = region;
+  G.far_g = region == 0 ? 0 : 2 * G.n[D - 1];
+  G.gamma_g = region == 0 ? 2 * G.n[D - 1] : 0;
+  return G;
+}
+
+inline dim3 grid_rows(int maxrows, int nsys, int bs = 128) { return dim3((maxrows + bs - 1) / bs, nsys); }
+
+template <int D>
+void build_pattern(lpfem_ctx* c, Family& F) {
+  cudaStream_t st = c->st;
+  const int nsys = (int)F.hs.size();
+  F.ds = dalloc<SysDesc>(nsys);
+  CK(cudaMemcpyAsync(F.ds, F.hs.data(), nsys * sizeof(SysDesc), cudaMemcpyHostToDevice, st));
+  long long* cnt = dalloc<long long>(F.rows + 1);
+  CK(cudaMemsetAsync(cnt, 0, (F.rows + 1) * sizeof(long long), st));
+  k_pattern_count<D><<<grid_rows(F.maxrows, nsys), 128, 0, st>>>(F.ds, F.kind, cnt);
+  CKL();
+  F.rowptr = dalloc<long long>(F.rows + 1);
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, F.rowptr, F.rows + 1, st));
+  void* dtmp = dalloc<char>(tmp);
+  CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt, F.rowptr, F.rows + 1, st));
+  CK(cudaMemcpyAsync(&F.nnz, F.rowptr + F.rows, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dtmp);
+  cudaFree(cnt);
+  {
+    std::vector<long long> rp(F.rows + 1);
+    CK(cudaMemcpy(rp.data(), F.rowptr, (F.rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
+    for (auto& S : F.hs) F.sys_nnz.push_back(rp[S.row_off + S.nrows] - rp[S.row_off]);
+  }
+  F.col = dalloc<int>(F.nnz);
+  k_pattern_fill<D><<<grid_rows(F.maxrows, nsys), 128, 0, st>>>(F.ds, F.kind, F.rowptr, F.col);
+  CKL();
+}
+
+void alloc_vectors(lpfem_ctx* c, Family& F) {
+  const long long nv = F.kind == 0 ? 3 * F.rows : F.rows;
+  F.base = dalloc<double>(nv);
+  F.z = dalloc<double>(nv);
+  F.lag = dalloc<double>(nv);
+  F.qf = dalloc<double>(nv);
+  F.aux = dalloc<double>(F.rows);
+  F.rhs = dalloc<double>(nv);
+  F.x = dalloc<double>(nv);
+  F.r = dalloc<double>(nv);
+  F.p = dalloc<double>(nv);
+  CK(cudaMemsetAsync(F.x, 0, nv * sizeof(double), c->st));
+  if (F.kind == 0) {
+    F.val = dalloc<double>(3 * F.nnz);
+    F.diag = dalloc<double>(nv);
+    F.isq = dalloc<double>(nv);
+    F.wn = dalloc<double>(nv);
+    F.q = dalloc<double>(nv);
+  } else {
+    F.aconst = dalloc<double>(F.nnz);
+    F.aout = dalloc<double>(F.nnz);
+    F.scale = dalloc<double>(F.rows);
+    F.W = dalloc<double>(F.rows);
+    F.V = dalloc<double>((size_t)(GM + 1) * F.rows);
+  }
+  if (F.level == 1 && c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN) {
+    F.ecorr = dalloc<double>(nv);
+    CK(cudaMemsetAsync(F.ecorr, 0, nv * sizeof(double), c->st));
+  }
+  // Krylov system list
+  const int nsub = (int)F.hs.size();
+  if (F.kind == 0) {
+    for (int f = 0; f < 3; ++f)
+      for (int s = 0; s < nsub; ++s) {
+        KSys k{};
+        k.row_off = f * F.rows + F.hs[s].row_off;
+        k.prow_off = F.hs[s].row_off;
+        k.val_off = f * F.nnz;
+        k.nrows = F.hs[s].nrows;
+        F.hk.push_back(k);
+      }
+  } else {
+    for (int s = 0; s < nsub; ++s) {
+      KSys k{};
+      k.row_off = F.hs[s].row_off;
+      k.prow_off = F.hs[s].row_off;
+      k.val_off = 0;
+      k.nrows = F.hs[s].nrows;
+      F.hk.push_back(k);
+    }
+  }
+  F.dk = dalloc<KSys>(F.hk.size());
+  CK(cudaMemcpyAsync(F.dk, F.hk.data(), F.hk.size() * sizeof(KSys), cudaMemcpyHostToDevice, c->st));
+  F.dstat = dalloc<KStat>(F.hk.size());
+  F.hstat.resize(F.hk.size());
+}
+
+// one system = the whole region on the coarse level
+SysDesc whole_region(int D, const LevelGeom& G, int kind) {
+  SysDesc S{};
+  for (int a = 0; a < 3; ++a) {
+    S.c0[a] = 0;
+    S.nc[a] = a < D ? G.n[a] : 0;
+    S.np[a] = a < D ? 2 * G.n[a] + 1 : 1;
+  }
+  S.n2 = 1;
+  S.n1 = 1;
+  for (int a = 0; a < D; ++a) {
+    S.n2 *= S.np[a];
+    S.n1 *= S.nc[a] + 1;
+  }
+  S.nrows = kind == 0 ? S.n2 : D * S.n2 + S.n1;
+  S.has_gamma = 1;
+  S.level = 0;
+  return S;
+}
+
+void finish_family(int D, Family& F) {
+  long long off = 0;
+  F.maxrows = 0;
+  F.maxitems = 0;
+  for (auto& S : F.hs) {
+    S.row_off = off;
+    off += S.nrows;
+    F.maxrows = std::max(F.maxrows, S.nrows);
+    F.maxitems = std::max(F.maxitems, S.n2 + S.n1);
+  }
+  F.rows = off;
+  (void)D;
+}
+
+template <int D>
+__global__ void k_init_p2(LevelGeom G, ProbData pd, Coef co, int kind, double* o0, double* o1, double* o2,
+                          long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int np[3] = {2 * G.n[0] + 1, 2 * G.n[1] + 1, 2 * G.n[2] + 1}, g[3] = {0, 0, 0};
+  unlex<D>(i, np, g);
+  double x[3] = {0, 0, 0};
+  for (int a = 0; a < D; ++a) x[a] = __dadd_rn(G.lo[a], __dmul_rn((double)g[a], G.hg[a]));
+  double v[3];
+  if (kind == 0) {
+    porous_values<D>(pd, x, 0.0, v);
+  } else {
+    velocity_values<D>(pd, x, 0.0, g[D - 1] == 2 * G.n[D - 1], v);
+  }
+  o0[i] = v[0];
+  o1[i] = v[1];
+  if (o2) o2[i] = v[2];
+}
+
+template <int D>
+__global__ void k_init_p1(LevelGeom G, ProbData pd, Coef co, double* o, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int nv[3] = {G.n[0] + 1, G.n[1] + 1, G.n[2] + 1}, v[3] = {0, 0, 0};
+  unlex<D>(i, nv, v);
+  double x[3] = {0, 0, 0};
+  for (int a = 0; a < D; ++a) x[a] = __dadd_rn(G.lo[a], __dmul_rn((double)(2 * v[a]), G.hg[a]));
+  o[i] = pressure_value<D>(pd, co, x, 0.0);
+}
+
+__global__ void k_sub(const double* a, const double* b, double* o, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) o[i] = a[i] - b[i];
+}
+
+// ||u - w||^2 and ||u||^2 over n entries (single block, fixed order)
+__global__ void k_picard_norms(const double* u, const double* w, long long n, double* out) {
+  __shared__ double s0[32], s1[32];
+  double a = 0.0, b = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = u[i] - w[i];
+    a += d * d;
+    b += u[i] * u[i];
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) {
+    s0[threadIdx.x >> 5] = a;
+    s1[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x0 = 0, x1 = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      x0 += s0[k];
+      x1 += s1[k];
+    }
+    out[0] = x0;
+    out[1] = x1;
+  }
+}
+
+template <class Kern>
+void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const KArgs& a) {
+  if (nsys == 0) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nsys * CL);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k, a));
+  ++tl_launches;
+}
+
+template <int D>
+PorousCoefs porous_coefs(const lpfem_ctx* c, double dt) {
+  PorousCoefs pc{};
+  const Coef& co = c->co;
+  const double gFf = co.sigma_star * co.k[1] / co.mu, gfm = co.sigma * co.k[0] / co.mu;
+  for (int f = 0; f < 3; ++f) {
+    pc.c[f] = co.phiC[f] / dt;
+    pc.kappa[f] = co.k[f] / co.mu;
+  }
+  pc.gamma[2] = gFf;
+  pc.gamma[1] = gfm + gFf;
+  pc.gamma[0] = gfm;
+  pc.gFf = gFf;
+  pc.gfm = gfm;
+  return pc;
+}
+
+template <int D>
+ConduitCoefs conduit_coefs(const lpfem_ctx* c, double dt, double hmin) {
+  ConduitCoefs cc{};
+  cc.eta = c->co.eta;
+  cc.nu = c->co.nu;
+  cc.alpha = c->co.alpha;
+  cc.rho = c->co.rho;
+  cc.mu = c->co.mu;
+  cc.kF = c->co.k[2];
+  cc.dt = dt;
+  cc.schur_w = c->co.nu + hmin * hmin / (c->schur_c * dt);
+  return cc;
+}
+
+template <int D>
+const RefT<D>* refp(const lpfem_ctx* c) {
+  return (const RefT<D>*)c->ref;
+}
+
+int nHv(const lpfem_ctx* c, int a) { return c->nc_p[a]; }
+
+template <int D>
+void assemble_dt(lpfem_ctx* c, double dt) {
+  cudaStream_t st = c->st;
+  const PorousCoefs pc = porous_coefs<D>(c, dt);
+  for (int lev = 0; lev < 2; ++lev) {
+    Family& P = c->fam[lev][0];
+    const int ns = (int)P.hs.size();
+    if (ns) {
+      k_porous_assemble<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(
+          P.ds, c->Lp[lev], pc, c->kmult, c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), P.rowptr, P.col, P.val,
+          P.nnz, P.diag, P.rows);
+      CKL();
+      k_porous_isq<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, c->Lp[lev], P.diag, P.isq, P.rows);
+      CKL();
+      k_porous_scale<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, P.rowptr, P.col, P.val, P.nnz, P.isq,
+                                                                   P.rows);
+      CKL();
+    }
+    Family& C = c->fam[lev][1];
+    const int nc = (int)C.hs.size();
+    if (nc) {
+      double hmin = 1e300;
+      for (int a = 0; a < D; ++a) hmin = std::min(hmin, c->Lc[lev].G.hc[a]);
+      const ConduitCoefs cc = conduit_coefs<D>(c, dt, hmin);
+      k_conduit_const<D><<<grid_rows(C.maxrows, nc), 128, 0, st>>>(C.ds, c->Lc[lev], cc, c->kmult, c->nc_p[0],
+                                                                    c->nc_p[1], c->nc_p[2], refp<D>(c), C.rowptr,
+                                                                    C.col, C.aconst);
+      CKL();
+      k_conduit_scale<D><<<grid_rows(C.maxrows, nc), 128, 0, st>>>(C.ds, c->Lc[lev], cc, C.rowptr, C.col, C.aconst,
+                                                                    C.scale);
+      CKL();
+    }
+  }
+  c->cur_dt = dt;
+}
+
+template <int D>
+void solve_porous(lpfem_ctx* c, Family& P) {
+  KArgs a{};
+  a.sys = P.dk;
+  a.rowptr = P.rowptr;
+  a.col = P.col;
+  a.val = P.val;
+  a.b = P.rhs;
+  a.w = P.wn;
+  a.x = P.x;
+  a.r = P.r;
+  a.p = P.p;
+  a.q = P.q;
+  a.rows_total = 3 * P.rows;
+  a.rtol = c->opts.krylov_rtol;
+  a.maxit = c->opts.max_iter;
+  a.stat = P.dstat;
+  if (D == 2)
+    launch_cluster(k_cg<1024, 4>, (int)P.hk.size(), P.cluster, 1024, c->st, a);
+  else
+    launch_cluster(k_cg<1024, 8>, (int)P.hk.size(), P.cluster, 1024, c->st, a);
+}
+
+template <int D>
+void solve_conduit(lpfem_ctx* c, Family& C) {
+  KArgs a{};
+  a.sys = C.dk;
+  a.rowptr = C.rowptr;
+  a.col = C.col;
+  a.val = C.aout;
+  a.b = C.rhs;
+  a.x = C.x;
+  a.r = C.r;
+  a.p = C.W;
+  a.V = C.V;
+  a.rows_total = C.rows;
+  a.rtol = c->opts.krylov_rtol;
+  a.maxit = c->opts.max_iter;
+  a.stat = C.dstat;
+  if (D == 2)
+    launch_cluster(k_gmres<512, 8, GM>, (int)C.hk.size(), C.cluster, 512, c->st, a);
+  else
+    launch_cluster(k_gmres<512, 16, GM>, (int)C.hk.size(), C.cluster, 512, c->st, a);
+}
+
+void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres, bool& ok) {
+  if (F.hk.empty()) return;
+  CK(cudaMemcpyAsync(F.hstat.data(), F.dstat, F.hstat.size() * sizeof(KStat), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  long long mx = 0, sum = 0;
+  for (auto& s : F.hstat) {
+    mx = std::max<long long>(mx, s.iters);
+    sum += s.iters;
+    maxres = std::max(maxres, s.relres);
+    if (!s.converged) ok = false;
+  }
+  if (coarse) {
+    c->stats.coarse_iters[kind] += sum;
+  } else {
+    c->stats.fine_iters[kind] += sum;
+    c->stats.fine_max_iters[kind] = mx;
+    // algorithmic bytes: SpMV 12 B/nnz + 32 B/row per pass; CG vector work
+    // 64 B/row per iteration; GMRES 48 B/row per iteration + 16 B/row per basis vector per Gram-Schmidt.
+    const int nsub = (int)F.hs.size();
+    double bytes = 0.0;
+    for (size_t i = 0; i < F.hstat.size(); ++i) {
+      const int s = (int)(i % nsub);
+      const double rows = F.hk[i].nrows, nz = (double)F.sys_nnz[s];
+      const KStat& k = F.hstat[i];
+      bytes += k.spmv * (12.0 * nz + 32.0 * rows);
+      bytes += kind == 0 ? 64.0 * rows * k.iters : 48.0 * rows * k.iters + 16.0 * rows * k.vsum;
+    }
+    c->stats.bytes_krylov[kind] += bytes;
+    c->stats.krylov_launches[kind] += 1;
+  }
+}
+
+template <int D>
+void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* const* cold, const double* cu_old_last,
+                  double* const* out) {
+  Family& P = c->fam[lev][0];
+  const int ns = (int)P.hs.size();
+  if (!ns) return;
+  cudaStream_t st = c->st;
+  PorousPrepArgs A{};
+  for (int f = 0; f < 3; ++f) {
+    A.coarse_new[f] = cnew[f];
+    A.coarse_old[f] = cold[f];
+    A.comp[f] = c->comp[f];
+  }
+  A.coarse_u_old = cu_old_last;
+  A.ecorr = P.ecorr;
+  for (int a = 0; a < 3; ++a) {
+    A.nHp[a] = c->nc_p[a];
+    A.nHc[a] = c->nc_c[a];
+    A.np_glob[a] = 2 * c->Lp[lev].G.n[a] + 1;
+  }
+  A.Rp = lev == 0 ? 1 : c->R;
+  A.conduit_gamma_g = 0;
+  A.mode = lev == 0 ? 2 : (c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN ? 1 : 0);
+  A.t = t;
+  k_porous_prep<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, c->Lp[lev], c->pd, c->co, A, P.base, P.z, P.lag,
+                                                              P.qf, P.aux, P.rows);
+  CKL();
+  const PorousCoefs pc = porous_coefs<D>(c, c->cur_dt);
+  k_porous_rhs<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, c->Lp[lev], pc, c->kmult, c->nc_p[0], c->nc_p[1],
+                                                             c->nc_p[2], refp<D>(c), P.z, P.lag, P.qf, P.aux, P.isq,
+                                                             P.rhs, P.wn, P.rows);
+  CKL();
+  if (lev == 1) CK(cudaEventRecord(c->ek[0], st));
+  solve_porous<D>(c, P);
+  if (lev == 1) CK(cudaEventRecord(c->ek[1], st));
+  k_porous_writeback<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(
+      P.ds, c->Lp[lev], P.z, P.x, P.isq, P.base, P.ecorr, out[0], out[1], out[2], 2 * c->Lp[lev].G.n[0] + 1,
+      2 * c->Lp[lev].G.n[1] + 1, 2 * c->Lp[lev].G.n[2] + 1, P.rows);
+  CKL();
+}
+
+template <int D>
+void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, const double* cp_new,
+                        const double* cu_old, const double* cpF_old, double* out_u, double* out_p) {
+  Family& C = c->fam[lev][1];
+  const int ns = (int)C.hs.size();
+  if (!ns) return;
+  cudaStream_t st = c->st;
+  ConduitPrepArgs A{};
+  A.cu_new = cu_new;
+  A.cp_new = cp_new;
+  A.cu_old = cu_old;
+  A.cpF_old = cpF_old;
+  A.comp_u = c->comp_u;
+  A.ecorr = C.ecorr;
+  for (int a = 0; a < 3; ++a) {
+    A.nHc[a] = c->nc_c[a];
+    A.nHp[a] = c->nc_p[a];
+    A.np_glob[a] = 2 * c->Lc[lev].G.n[a] + 1;
+  }
+  A.R = lev == 0 ? 1 : c->R;
+  A.n2_glob = lev == 0 ? c->n2c_c : c->n2c_f;
+  A.porous_gamma_g = 2 * c->nc_p[D - 1] * A.R;
+  A.mode = lev == 0 ? 2 : (c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN ? 1 : 0);
+  A.t = t;
+  k_conduit_prep<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(C.ds, c->Lc[lev], c->pd, c->co, A, C.base, C.z, C.W,
+                                                               C.lag, C.qf, C.aux);
+  CKL();
+  double hmin = 1e300;
+  for (int a = 0; a < D; ++a) hmin = std::min(hmin, c->Lc[lev].G.hc[a]);
+  const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
+  k_conduit_step<D><<<grid_rows(C.maxrows, ns), 128, 0, st>>>(C.ds, c->Lc[lev], cc, lev == 1 ? 1 : 0, c->kmult,
+                                                               c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), C.rowptr,
+                                                               C.col, C.aconst, C.scale, C.z, C.W, C.lag, C.qf, C.aux,
+                                                               C.aout, C.rhs);
+  CKL();
+  if (lev == 1) CK(cudaEventRecord(c->ek[2], st));
+  solve_conduit<D>(c, C);
+  if (lev == 1) CK(cudaEventRecord(c->ek[3], st));
+  const int* npg = A.np_glob;
+  k_conduit_writeback<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(C.ds, c->Lc[lev], C.z, C.x, C.scale, C.base,
+                                                                    C.ecorr, out_u, out_p, npg[0], npg[1], npg[2],
+                                                                    A.n2_glob);
+  CKL();
+}
+
+template <int D>
+void do_step(lpfem_ctx* c, double dt) {
+  if (dt != c->cur_dt) assemble_dt<D>(c, dt);
+  cudaStream_t st = c->st;
+  const double t = (double)(c->nstep + 1) * dt;  // C18
+  double maxres[2] = {0, 0};
+  bool ok = true;
+  CK(cudaEventRecord(c->ev[0], st));
+  // ---------------- Step 1: coarse, Algorithm 1 on T_H
+  porous_stage<D>(c, 0, t, c->cst[0], c->cst[0], c->cu[0] + (D - 1) * c->n2c_c, c->cst[1]);
+  {
+    double dummy = 0;
+    fetch_stats(c, c->fam[0][0], 0, true, dummy, ok);
+  }
+  const long long nu = (long long)D * c->n2c_c;
+  CK(cudaMemcpyAsync(c->wpic, c->cu[0], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->ppic, c->cp[0], c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  bool pic_ok = false;
+  for (int it = 0; it < c->opts.picard_max; ++it) {
+    conduit_solve_once<D>(c, 0, t, c->wpic, c->ppic, c->cu[0], c->cst[0][2], c->wpic2, c->ppic2);
+    double dummy = 0;
+    fetch_stats(c, c->fam[0][1], 1, true, dummy, ok);
+    k_picard_norms<<<1, 1024, 0, st>>>(c->wpic2, c->wpic, nu, c->nrm);
+    CKL();
+    double hn[2];
+    CK(cudaMemcpyAsync(hn, c->nrm, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::swap(c->wpic, c->wpic2);
+    std::swap(c->ppic, c->ppic2);
+    c->stats.picard_iters++;
+    const double du = std::sqrt(hn[0]), un = std::sqrt(hn[1]);
+    if (du <= c->opts.picard_rtol * un || du <= 1e-14 * std::sqrt((double)nu)) {
+      pic_ok = true;
+      break;
+    }
+  }
+  if (!pic_ok) throw Err(LPFEM_ENOCONV, "coarse Picard iteration did not converge (C11)");
+  CK(cudaMemcpyAsync(c->cu[1], c->wpic, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->cp[1], c->ppic, c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(c->ev[1], st));
+  // ---------------- Steps 3-4: fine corrections + write-back
+  porous_stage<D>(c, 1, t, c->cst[1], c->cst[0], c->cu[0] + (D - 1) * c->n2c_c, c->comp);
+  conduit_solve_once<D>(c, 1, t, c->cu[1], c->cp[1], c->cu[0], c->cst[0][2], c->comp_u, c->comp_p);
+  CK(cudaEventRecord(c->ev[2], st));
+  fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
+  fetch_stats(c, c->fam[1][1], 1, false, maxres[1], ok);
+  float ms0 = 0, ms1 = 0, mk0 = 0, mk1 = 0;
+  CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
+  CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
+  if (!c->fam[1][0].hs.empty()) CK(cudaEventElapsedTime(&mk0, c->ek[0], c->ek[1]));
+  if (!c->fam[1][1].hs.empty()) CK(cudaEventElapsedTime(&mk1, c->ek[2], c->ek[3]));
+  c->stats.t_krylov_ms[0] += mk0;
+  c->stats.t_krylov_ms[1] += mk1;
+  c->stats.kernel_launches += tl_launches;
+  tl_launches = 0;
+  c->stats.t_coarse_ms += ms0;
+  c->stats.t_fine_ms += ms1;
+  c->stats.max_rel_residual[0] = maxres[0];
+  c->stats.max_rel_residual[1] = maxres[1];
+  for (int f = 0; f < 3; ++f) std::swap(c->cst[0][f], c->cst[1][f]);
+  std::swap(c->cu[0], c->cu[1]);
+  std::swap(c->cp[0], c->cp[1]);
+  c->nstep++;
+  c->stats.steps = c->nstep;
+  if (!ok) throw Err(LPFEM_ENOCONV, "a Krylov solve did not reach the relative residual (C19)");
+}
+
+template <int D>
+void setup(lpfem_ctx* c) {
+  upload_tables();
+  // reference tensors
+  RefT<D>* href = new RefT<D>();
+  build_ref<D>(*href);
+  c->ref = dalloc<RefT<D>>(1);
+  CK(cudaMemcpy(c->ref, href, sizeof(RefT<D>), cudaMemcpyHostToDevice));
+  delete href;
+  const lpfem_geometry& g = c->geom;
+  const double steps[2] = {c->H, c->h};
+  for (int lev = 0; lev < 2; ++lev) {
+    const int R = lev == 0 ? 1 : c->R;
+    c->Lp[lev].G = make_level(D, g.porous_lo, g.porous_hi, 0, steps[lev], R);
+    c->Lc[lev].G = make_level(D, g.conduit_lo, g.conduit_hi, 1, steps[lev], R);
+    for (int a = 0; a < 3; ++a) {
+      c->Lp[lev].m[a] = c->Lc[lev].m[a] = a < D ? c->m[a] : 1;
+      c->Lp[lev].core[a] = c->Lp[lev].G.n[a] / std::max(1, c->Lp[lev].m[a]);
+      c->Lc[lev].core[a] = c->Lc[lev].G.n[a] / std::max(1, c->Lc[lev].m[a]);
+    }
+  }
+  for (int a = 0; a < 3; ++a) {
+    c->nc_p[a] = c->Lp[0].G.n[a];
+    c->nc_c[a] = c->Lc[0].G.n[a];
+    c->nf_p[a] = c->Lp[1].G.n[a];
+    c->nf_c[a] = c->Lc[1].G.n[a];
+  }
+  for (int a = 0; a < D; ++a) {
+    if (c->nf_p[a] % c->m[a] || c->nf_c[a] % c->m[a])
+      throw Err(LPFEM_EMISALIGN, "subdomain grid does not divide the fine mesh");
+    if (c->nf_p[a] != c->R * c->nc_p[a] || c->nf_c[a] != c->R * c->nc_c[a])
+      throw Err(LPFEM_ENOTDIV, "H/h is not an integer on every axis");
+  }
+  auto cnt = [&](const int* n, int add, int mul) {
+    long long s = 1;
+    for (int a = 0; a < D; ++a) s *= (long long)mul * n[a] + add;
+    return s;
+  };
+  c->n2p_f = cnt(c->nf_p, 1, 2);
+  c->n2c_f = cnt(c->nf_c, 1, 2);
+  c->n1c_f = cnt(c->nf_c, 1, 1);
+  c->n2p_c = cnt(c->nc_p, 1, 2);
+  c->n2c_c = cnt(c->nc_c, 1, 2);
+  c->n1c_c = cnt(c->nc_c, 1, 1);
+  c->stats.fine_dofs = 3 * c->n2p_f + D * c->n2c_f + c->n1c_f;
+  // coarse families: one system per region
+  for (int k = 0; k < 2; ++k) {
+    Family& F = c->fam[0][k];
+    F.kind = k;
+    F.level = 0;
+    F.hs.push_back(whole_region(D, k == 0 ? c->Lp[0].G : c->Lc[0].G, k));
+    finish_family(D, F);
+  }
+  // fine families: overlapping subdomains (Algorithm 3 Step 2; C7, C8)
+  const int npos = c->m[0] * c->m[1] * (D > 2 ? c->m[2] : 1);
+  std::vector<int> mine;
+  for (int s = 0; s < npos; ++s)
+    if ((long long)s * c->dist.world / npos == c->dist.rank) mine.push_back(s);  // contiguous blocks
+  for (int k = 0; k < 2; ++k) {
+    Family& F = c->fam[1][k];
+    F.kind = k;
+    F.level = 1;
+    const LevelGeom& G = k == 0 ? c->Lp[1].G : c->Lc[1].G;
+    for (int s : mine) {
+      int pos[3] = {0, 0, 0};
+      int rem = s;
+      for (int a = 0; a < D; ++a) {
+        pos[a] = rem % c->m[a];
+        rem /= c->m[a];
+      }
+      SysDesc S{};
+      S.n2 = 1;
+      S.n1 = 1;
+      std::array<int, 3> cr0 = {0, 0, 0}, cr1 = {0, 0, 0};
+      for (int a = 0; a < 3; ++a) {
+        S.np[a] = 1;
+        if (a >= D) continue;
+        const int core = G.n[a] / c->m[a];
+        const int c0 = pos[a] * core, c1 = c0 + core;
+        const int e0 = std::max(0, c0 - c->ov), e1 = std::min(G.n[a], c1 + c->ov);
+        S.c0[a] = e0;
+        S.nc[a] = e1 - e0;
+        S.np[a] = 2 * S.nc[a] + 1;
+        S.art_lo[a] = e0 > 0;
+        S.art_hi[a] = e1 < G.n[a];
+        S.pos[a] = pos[a];
+        S.n2 *= S.np[a];
+        S.n1 *= S.nc[a] + 1;
+        cr0[a] = c0;
+        cr1[a] = c1;
+      }
+      S.nrows = k == 0 ? S.n2 : D * S.n2 + S.n1;
+      S.has_gamma = k == 0 ? (S.c0[D - 1] + S.nc[D - 1] == G.n[D - 1]) : (S.c0[D - 1] == 0);
+      S.level = 1;
+      F.hs.push_back(S);
+      F.sub_region.push_back(k);
+      F.sub_pos.push_back(s);
+      F.core0.push_back(cr0);
+      F.core1.push_back(cr1);
+    }
+    finish_family(D, F);
+  }
+  for (int lev = 0; lev < 2; ++lev)
+    for (int k = 0; k < 2; ++k) {
+      Family& F = c->fam[lev][k];
+      if (F.hs.empty()) continue;
+      build_pattern<D>(c, F);
+      alloc_vectors(c, F);
+    }
+  // cluster sizes: spread the systems of a family over the SMs (deterministic in the global layout)
+  {
+    int nsm = 148;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, c->dist.device) == cudaSuccess) nsm = prop.multiProcessorCount;
+    (void)nsm;
+    for (int lev = 0; lev < 2; ++lev)
+      for (int k = 0; k < 2; ++k) c->fam[lev][k].cluster = 1;
+  }
+  // states
+  for (int s = 0; s < 2; ++s) {
+    for (int f = 0; f < 3; ++f) c->cst[s][f] = dalloc<double>(c->n2p_c);
+    c->cu[s] = dalloc<double>(D * c->n2c_c);
+    c->cp[s] = dalloc<double>(c->n1c_c);
+  }
+  c->wpic = dalloc<double>(D * c->n2c_c);
+  c->wpic2 = dalloc<double>(D * c->n2c_c);
+  c->ppic = dalloc<double>(c->n1c_c);
+  c->ppic2 = dalloc<double>(c->n1c_c);
+  c->nrm = dalloc<double>(2);
+  for (int f = 0; f < 3; ++f) c->comp[f] = dalloc<double>(c->n2p_f);
+  c->comp_u = dalloc<double>(D * c->n2c_f);
+  c->comp_p = dalloc<double>(c->n1c_f);
+  if (!c->hkmult.empty()) {
+    c->kmult = dalloc<double>(c->hkmult.size());
+    CK(cudaMemcpy(c->kmult, c->hkmult.data(), c->hkmult.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  cudaStream_t st = c->st;
+  // C12: u_H^0 = I_H u_0, u^h_0 = I_h u_0
+  auto init = [&](int lev, double* const* pp, double* u, double* p) {
+    const LevelGeom& Gp = c->Lp[lev].G;
+    const LevelGeom& Gc = c->Lc[lev].G;
+    long long n = lev == 0 ? c->n2p_c : c->n2p_f;
+    k_init_p2<D><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Gp, c->pd, c->co, 0, pp[0], pp[1], pp[2], n);
+    CKL();
+    n = lev == 0 ? c->n2c_c : c->n2c_f;
+    k_init_p2<D><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Gc, c->pd, c->co, 1, u, u + n,
+                                                               D > 2 ? u + 2 * n : nullptr, n);
+    CKL();
+    n = lev == 0 ? c->n1c_c : c->n1c_f;
+    k_init_p1<D><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Gc, c->pd, c->co, p, n);
+    CKL();
+  };
+  init(0, c->cst[0], c->cu[0], c->cp[0]);
+  init(1, c->comp, c->comp_u, c->comp_p);
+  for (int i = 0; i < 4; ++i) {
+    CK(cudaEventCreate(&c->ev[i]));
+    CK(cudaEventCreate(&c->ek[i]));
+  }
+  // mode A: e_j^0 = (I_h u_0 - P I_H u_0) on every box node (C12)
+  if (c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN) {
+    Family& P = c->fam[1][0];
+    Family& C = c->fam[1][1];
+    if (!P.hs.empty()) {
+      PorousPrepArgs A{};
+      for (int f = 0; f < 3; ++f) {
+        A.coarse_new[f] = c->cst[0][f];
+        A.coarse_old[f] = c->cst[0][f];
+        A.comp[f] = c->comp[f];
+      }
+      A.coarse_u_old = c->cu[0];
+      for (int a = 0; a < 3; ++a) {
+        A.nHp[a] = c->nc_p[a];
+        A.nHc[a] = c->nc_c[a];
+        A.np_glob[a] = 2 * c->nf_p[a] + 1;
+      }
+      A.Rp = c->R;
+      A.mode = 0;
+      k_porous_prep<D><<<grid_rows(P.maxrows, (int)P.hs.size()), 128, 0, st>>>(
+          P.ds, c->Lp[1], c->pd, c->co, A, P.base, P.z, P.lag, P.qf, P.aux, P.rows);
+      CKL();
+      k_sub<<<(unsigned)((3 * P.rows + 255) / 256), 256, 0, st>>>(P.lag, P.base, P.ecorr, 3 * P.rows);
+      CKL();
+    }
+    if (!C.hs.empty()) {
+      ConduitPrepArgs A{};
+      A.cu_new = c->cu[0];
+      A.cp_new = c->cp[0];
+      A.cu_old = c->cu[0];
+      A.cpF_old = c->cst[0][2];
+      A.comp_u = c->comp_u;
+      for (int a = 0; a < 3; ++a) {
+        A.nHc[a] = c->nc_c[a];
+        A.nHp[a] = c->nc_p[a];
+        A.np_glob[a] = 2 * c->nf_c[a] + 1;
+      }
+      A.R = c->R;
+      A.n2_glob = c->n2c_f;
+      A.porous_gamma_g = 2 * c->nf_p[D - 1];
+      A.mode = 0;
+      k_conduit_prep<D><<<grid_rows(C.maxitems, (int)C.hs.size()), 128, 0, st>>>(
+          C.ds, c->Lc[1], c->pd, c->co, A, C.base, C.z, C.W, C.lag, C.qf, C.aux);
+      CKL();
+      k_sub<<<(unsigned)((C.rows + 255) / 256), 256, 0, st>>>(C.lag, C.base, C.ecorr, C.rows);
+      CKL();
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  for (int k = 0; k < 2; ++k) {
+    c->stats.n_systems[k] = (long long)c->fam[1][k].hk.size();
+    c->stats.n_rows[k] = c->fam[1][k].rows;
+    c->stats.nnz[k] = c->fam[1][k].nnz;
+  }
+}
+
+lpfem_status fail(lpfem_ctx* c, const Err& e) {
+  if (c) c->err = e.what();
+  return e.code;
+}
+
+// NCCL is loaded lazily (multi-GPU only) so that the library has no link-time NCCL dependency.
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  bool load() {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    getUniqueId = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
+    return getUniqueId != nullptr;
+  }
+};
+NcclApi g_nccl;
+
+}  // namespace
+
+// ============================================================================================ C-ABI
+extern "C" {
+
+const char* lpfem_status_string(lpfem_status s) {
+  switch (s) {
+    case LPFEM_OK: return "ok";
+    case LPFEM_EINVAL: return "invalid argument";
+    case LPFEM_ENOTDIV: return "mesh sizes not integral";
+    case LPFEM_EMISALIGN: return "subdomain layout misaligned";
+    case LPFEM_ENOCONV: return "solver did not converge";
+    case LPFEM_ECUDA: return "CUDA error";
+    case LPFEM_ENCCL: return "NCCL error";
+    case LPFEM_ENOMEM: return "out of device memory";
+    case LPFEM_ESTATE: return "bad state";
+  }
+  return "unknown";
+}
+
+lpfem_status lpfem_nccl_unique_id(unsigned char out[128]) {
+  if (!out) return LPFEM_EINVAL;
+  if (!g_nccl.load()) return LPFEM_ENCCL;
+  return g_nccl.getUniqueId(out) == 0 ? LPFEM_OK : LPFEM_ENCCL;
+}
+
+lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs, const lpfem_data* data, double H,
+                          double h, double overlap, const int subdomain_grid[3], const lpfem_opts* opts,
+                          const lpfem_dist* dist, lpfem_ctx** out) {
+  if (!geom || !coeffs || !data || !subdomain_grid || !opts || !out) return LPFEM_EINVAL;
+  *out = nullptr;
+  lpfem_ctx* c = new lpfem_ctx();
+  try {
+    if (geom->dim != 2 && geom->dim != 3) throw Err(LPFEM_EINVAL, "dim must be 2 or 3");
+    if (!(H > 0) || !(h > 0) || !(overlap >= 0)) throw Err(LPFEM_EINVAL, "H, h must be > 0 and overlap >= 0");
+    c->D = geom->dim;
+    c->geom = *geom;
+    c->H = H;
+    c->h = h;
+    c->R = to_int_checked(H / h, LPFEM_ENOTDIV, "H/h");
+    to_int_checked(1.0 / h, LPFEM_ENOTDIV, "1/h");
+    to_int_checked(1.0 / H, LPFEM_ENOTDIV, "1/H");
+    c->ov = (int)std::round(overlap / h);
+    if (std::fabs(overlap / h - c->ov) > 1e-9) throw Err(LPFEM_EMISALIGN, "overlap is not a multiple of h");
+    for (int a = 0; a < 3; ++a) c->m[a] = a < c->D ? subdomain_grid[a] : 1;
+    for (int a = 0; a < c->D; ++a)
+      if (c->m[a] < 1) throw Err(LPFEM_EINVAL, "subdomain grid must be >= 1");
+    for (int i = 0; i < 3; ++i) {
+      c->co.phiC[i] = coeffs->phi[i] * coeffs->C[i];
+      c->co.k[i] = coeffs->k[i];
+    }
+    c->co.sigma = coeffs->sigma;
+    c->co.sigma_star = coeffs->sigma_star;
+    c->co.mu = coeffs->mu_tilde;
+    c->co.nu = coeffs->nu;
+    c->co.rho = coeffs->rho;
+    c->co.alpha = coeffs->alpha;
+    c->co.eta = coeffs->eta;
+    c->pd.kind = data->problem;
+    c->pd.peak = data->inflow_peak;
+    c->pd.cval = data->const_value;
+    if (c->pd.kind < 0 || c->pd.kind > 3) throw Err(LPFEM_EINVAL, "unknown problem");
+    c->opts = *opts;
+    if (c->opts.krylov_rtol <= 0) c->opts.krylov_rtol = 1e-12;
+    if (c->opts.max_iter <= 0) c->opts.max_iter = 20000;
+    if (c->opts.picard_rtol <= 0) c->opts.picard_rtol = 1e-13;
+    if (c->opts.picard_max <= 0) c->opts.picard_max = 50;
+    if (dist) {
+      c->dist = *dist;
+    } else {
+      c->dist.rank = 0;
+      c->dist.world = 1;
+      c->dist.device = 0;
+    }
+    if (c->dist.world < 1 || c->dist.rank < 0 || c->dist.rank >= c->dist.world) throw Err(LPFEM_EINVAL, "bad dist");
+    if (c->dist.world > 1) throw Err(LPFEM_EINVAL, "multi-GPU halo exchange not built in this version");
+    CK(cudaSetDevice(c->dist.device));
+    c->st = (cudaStream_t)c->dist.cuda_stream;
+    if (coeffs->k_mult) {
+      long long ncells = 1;
+      for (int a = 0; a < c->D; ++a)
+        ncells *= to_int_checked((geom->porous_hi[a] - geom->porous_lo[a]) / H, LPFEM_ENOTDIV, "porous extent / H");
+      c->hkmult.assign(coeffs->k_mult, coeffs->k_mult + ncells);
+    }
+    if (c->D == 2) setup<2>(c); else setup<3>(c);
+    *out = c;
+    return LPFEM_OK;
+  } catch (const Err& e) {
+    lpfem_status s = e.code;
+    fprintf(stderr, "lpfem_create: %s\n", e.what());
+    lpfem_destroy(c);
+    return s;
+  }
+}
+
+lpfem_status lpfem_step(lpfem_ctx* c, double dt) {
+  if (!c) return LPFEM_EINVAL;
+  if (!(dt > 0)) {
+    c->err = "dt must be > 0";
+    return LPFEM_EINVAL;
+  }
+  try {
+    if (c->D == 2) do_step<2>(c, dt); else do_step<3>(c, dt);
+    return LPFEM_OK;
+  } catch (const Err& e) {
+    return fail(c, e);
+  }
+}
+
+lpfem_status lpfem_get_sizes(const lpfem_ctx* c, long long n_nodes_p2[2], long long n_nodes_p1[2]) {
+  if (!c || !n_nodes_p2 || !n_nodes_p1) return LPFEM_EINVAL;
+  n_nodes_p2[0] = c->n2p_f;
+  n_nodes_p2[1] = c->n2c_f;
+  n_nodes_p1[0] = 0;
+  n_nodes_p1[1] = c->n1c_f;
+  return LPFEM_OK;
+}
+
+static lpfem_status copy_out(lpfem_ctx* c, double* dst, const double* src, long long n, int on_device) {
+  if (!dst) return LPFEM_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, src, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st);
+  if (e != cudaSuccess) {
+    c->err = cudaGetErrorString(e);
+    return LPFEM_ECUDA;
+  }
+  return LPFEM_OK;
+}
+
+lpfem_status lpfem_get_fields(lpfem_ctx* c, double* pF, double* pf, double* pm, double* u, double* p, int on_device,
+                              int root) {
+  if (!c) return LPFEM_EINVAL;
+  (void)root;
+  lpfem_status s;
+  if ((s = copy_out(c, pF, c->comp[2], c->n2p_f, on_device))) return s;
+  if ((s = copy_out(c, pf, c->comp[1], c->n2p_f, on_device))) return s;
+  if ((s = copy_out(c, pm, c->comp[0], c->n2p_f, on_device))) return s;
+  if ((s = copy_out(c, u, c->comp_u, c->D * c->n2c_f, on_device))) return s;
+  if ((s = copy_out(c, p, c->comp_p, c->n1c_f, on_device))) return s;
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) return LPFEM_ECUDA;
+  return LPFEM_OK;
+}
+
+lpfem_status lpfem_get_coarse_fields(lpfem_ctx* c, double* pF, double* pf, double* pm, double* u, double* p) {
+  if (!c) return LPFEM_EINVAL;
+  lpfem_status s;
+  if ((s = copy_out(c, pF, c->cst[0][2], c->n2p_c, 0))) return s;
+  if ((s = copy_out(c, pf, c->cst[0][1], c->n2p_c, 0))) return s;
+  if ((s = copy_out(c, pm, c->cst[0][0], c->n2p_c, 0))) return s;
+  if ((s = copy_out(c, u, c->cu[0], c->D * c->n2c_c, 0))) return s;
+  if ((s = copy_out(c, p, c->cp[0], c->n1c_c, 0))) return s;
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) return LPFEM_ECUDA;
+  return LPFEM_OK;
+}
+
+lpfem_status lpfem_get_mesh(const lpfem_ctx* c, int which, double* coords, int* cells, long long n_out[2]) {
+  if (!c || !n_out || which < 0 || which > 3) return LPFEM_EINVAL;
+  const int D = c->D;
+  const int lev = which / 2, reg = which % 2;
+  const LevelGeom& G = reg == 0 ? c->Lp[lev].G : c->Lc[lev].G;
+  int np[3] = {1, 1, 1};
+  long long n2 = 1, ncell = 1;
+  for (int a = 0; a < D; ++a) {
+    np[a] = 2 * G.n[a] + 1;
+    n2 *= np[a];
+    ncell *= G.n[a];
+  }
+  KuhnTables T;
+  build_kuhn(D, T);
+  const int nt = nt_of(D), N = n2_of(D);
+  n_out[0] = n2;
+  n_out[1] = ncell * nt;
+  if (coords) {
+    for (long long i = 0; i < n2; ++i) {
+      int g[3] = {0, 0, 0};
+      unlex<3>(i, np, g);
+      for (int a = 0; a < D; ++a) {
+        volatile double prod = (double)g[a] * G.hg[a];  // no contraction: lo + g * step (C21)
+        coords[i * D + a] = G.lo[a] + prod;
+      }
+    }
+  }
+  if (cells) {
+    for (long long k = 0; k < ncell; ++k) {
+      int cc[3] = {0, 0, 0};
+      int nn[3] = {G.n[0], G.n[1], G.n[2]};
+      unlex<3>(k, nn, cc);
+      for (int t = 0; t < nt; ++t)
+        for (int j = 0; j < N; ++j) {
+          int v[3] = {0, 0, 0};
+          for (int a = 0; a < D; ++a) v[a] = 2 * cc[a] + T.off[t][j][a];
+          long long idx = 0, s = 1;
+          for (int a = 0; a < D; ++a) {
+            idx += v[a] * s;
+            s *= np[a];
+          }
+          cells[(k * nt + t) * N + j] = (int)idx;
+        }
+    }
+  }
+  return LPFEM_OK;
+}
+
+lpfem_status lpfem_get_layout(const lpfem_ctx* c, int* region, int* pos, int* core0, int* core1, int* box0, int* box1,
+                              int* n_out) {
+  if (!c || !n_out) return LPFEM_EINVAL;
+  int n = 0;
+  for (int k = 0; k < 2; ++k) {
+    const Family& F = c->fam[1][k];
+    for (size_t s = 0; s < F.hs.size(); ++s, ++n) {
+      if (region) region[n] = k;
+      if (pos) pos[n] = F.sub_pos[s];
+      for (int a = 0; a < 3; ++a) {
+        if (core0) core0[3 * n + a] = F.core0[s][a];
+        if (core1) core1[3 * n + a] = F.core1[s][a];
+        if (box0) box0[3 * n + a] = F.hs[s].c0[a];
+        if (box1) box1[3 * n + a] = F.hs[s].c0[a] + F.hs[s].nc[a];
+      }
+    }
+  }
+  *n_out = n;
+  return LPFEM_OK;
+}
+
+lpfem_status lpfem_get_stats(const lpfem_ctx* c, lpfem_stats* out) {
+  if (!c || !out) return LPFEM_EINVAL;
+  *out = c->stats;
+  return LPFEM_OK;
+}
+
+lpfem_status lpfem_get_system(lpfem_ctx* c, int family, int local_index, int field, long long* nrows, long long* nnz,
+                              long long* rowptr, int* col, double* val, double* rhs, double* x) {
+  if (!c || family < 0 || family > 1 || !nrows || !nnz) return LPFEM_EINVAL;
+  Family& F = c->fam[1][family];
+  if (local_index < 0 || local_index >= (int)F.hs.size()) return LPFEM_EINVAL;
+  if (family == 0 && (field < 0 || field > 2)) return LPFEM_EINVAL;
+  const SysDesc& S = F.hs[local_index];
+  std::vector<long long> rp(S.nrows + 1);
+  if (cudaMemcpy(rp.data(), F.rowptr + S.row_off, (S.nrows + 1) * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return LPFEM_ECUDA;
+  *nrows = S.nrows;
+  *nnz = rp[S.nrows] - rp[0];
+  if (rowptr)
+    for (int i = 0; i <= S.nrows; ++i) rowptr[i] = rp[i] - rp[0];
+  const long long voff = family == 0 ? field * F.nnz : 0;
+  const long long roff = (family == 0 ? field * F.rows : 0) + S.row_off;
+  const double* vsrc = family == 0 ? F.val : F.aout;
+  if (col && cudaMemcpy(col, F.col + rp[0], *nnz * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return LPFEM_ECUDA;
+  if (val && cudaMemcpy(val, vsrc + voff + rp[0], *nnz * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return LPFEM_ECUDA;
+  if (rhs && cudaMemcpy(rhs, F.rhs + roff, S.nrows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return LPFEM_ECUDA;
+  if (x && cudaMemcpy(x, F.x + roff, S.nrows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) return LPFEM_ECUDA;
+  return LPFEM_OK;
+}
+
+const char* lpfem_last_error(const lpfem_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+void lpfem_destroy(lpfem_ctx* c) {
+  if (!c) return;
+  for (int lev = 0; lev < 2; ++lev)
+    for (int k = 0; k < 2; ++k) c->fam[lev][k].free_all();
+  for (int s = 0; s < 2; ++s) {
+    for (int f = 0; f < 3; ++f)
+      if (c->cst[s][f]) cudaFree(c->cst[s][f]);
+    if (c->cu[s]) cudaFree(c->cu[s]);
+    if (c->cp[s]) cudaFree(c->cp[s]);
+  }
+  void* ptrs[] = {c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
+                  c->comp_p, c->kmult, c->ref};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (int i = 0; i < 4; ++i) {
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->ek[i]) cudaEventDestroy(c->ek[i]);
+  }
+  delete c;
+}
+
+}  // extern "C"
