@@ -36,7 +36,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", SRC, "-ldl"]
+    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", SRC, "-ldl", "-L/usr/local/cuda/lib64", "-lcusolver",
+           "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)

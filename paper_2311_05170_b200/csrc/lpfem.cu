@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
+#include <cusolverDn.h>
 
 #include "../../include/lpfem.h"
 #include "assembly.cuh"
@@ -127,6 +128,11 @@ struct lpfem_ctx {
   long long nstep = 0;
   double cur_dt = -1.0;
   double schur_c = 1.0;
+  // coarse Navier-Stokes: dense LU on the device (cuSOLVER), Step 1 dependency (C11)
+  cusolverDnHandle_t sol = nullptr;
+  double *dense = nullptr, *dwork = nullptr;
+  int *piv = nullptr, *dinfo = nullptr;
+  int lwork = 0;
 };
 
 namespace {
@@ -362,7 +368,8 @@ __global__ void k_init_p2(LevelGeom G, ProbData pd, Coef co, int kind, double* o
   if (kind == 0) {
     porous_values<D>(pd, x, 0.0, v);
   } else {
-    velocity_values<D>(pd, x, 0.0, g[D - 1] == 2 * G.n[D - 1], v);
+    // initial velocity I_h u_0: the injection problems start from rest (C16), the inflow acts from t_1 on
+    velocity_values<D>(pd, x, 0.0, false, v);
   }
   o0[i] = v[0];
   o1[i] = v[1];
@@ -378,6 +385,19 @@ __global__ void k_init_p1(LevelGeom G, ProbData pd, Coef co, double* o, long lon
   double x[3] = {0, 0, 0};
   for (int a = 0; a < D; ++a) x[a] = __dadd_rn(G.lo[a], __dmul_rn((double)(2 * v[a]), G.hg[a]));
   o[i] = pressure_value<D>(pd, co, x, 0.0);
+}
+
+// dense column-major copy of the single coarse saddle system A' (fixed rows/columns -> identity)
+__global__ void k_csr_to_dense(const long long* __restrict__ rowptr, const int* __restrict__ col,
+                               const double* __restrict__ val, const double* __restrict__ s, int n,
+                               double* __restrict__ A) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  if (s[r] == 0.0) {
+    A[(long long)r * n + r] = 1.0;
+    return;
+  }
+  for (long long q = rowptr[r]; q < rowptr[r + 1]; ++q) A[(long long)col[q] * n + r] = val[q];
 }
 
 __global__ void k_sub(const double* a, const double* b, double* o, long long n) {
@@ -658,9 +678,26 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
                                                                C.col, C.aconst, C.scale, C.z, C.W, C.lag, C.qf, C.aux,
                                                                C.aout, C.rhs);
   CKL();
-  if (lev == 1) CK(cudaEventRecord(c->ek[2], st));
-  solve_conduit<D>(c, C);
-  if (lev == 1) CK(cudaEventRecord(c->ek[3], st));
+  if (lev == 0) {
+    const int n = (int)C.rows;
+    CK(cudaMemsetAsync(c->dense, 0, (size_t)n * n * sizeof(double), st));
+    k_csr_to_dense<<<(n + 127) / 128, 128, 0, st>>>(C.rowptr, C.col, C.aout, C.scale, n, c->dense);
+    CKL();
+    CK(cudaMemcpyAsync(C.x, C.rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (cusolverDnDgetrf(c->sol, n, n, c->dense, n, c->dwork, c->piv, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
+      throw Err(LPFEM_ECUDA, "cusolverDnDgetrf");
+    if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, 1, c->dense, n, c->piv, C.x, n, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
+      throw Err(LPFEM_ECUDA, "cusolverDnDgetrs");
+    KStat ks{};
+    ks.iters = 1;
+    ks.converged = 1;
+    ks.spmv = 1;
+    CK(cudaMemcpyAsync(C.dstat, &ks, sizeof(KStat), cudaMemcpyHostToDevice, st));
+  } else {
+    if (lev == 1) CK(cudaEventRecord(c->ek[2], st));
+    solve_conduit<D>(c, C);
+    if (lev == 1) CK(cudaEventRecord(c->ek[3], st));
+  }
   const int* npg = A.np_glob;
   k_conduit_writeback<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(C.ds, c->Lc[lev], C.z, C.x, C.scale, C.base,
                                                                     C.ecorr, out_u, out_p, npg[0], npg[1], npg[2],
@@ -889,6 +926,17 @@ void setup(lpfem_ctx* c) {
   };
   init(0, c->cst[0], c->cu[0], c->cp[0]);
   init(1, c->comp, c->comp_u, c->comp_p);
+  {
+    const int n = (int)c->fam[0][1].rows;
+    if (cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
+    cusolverDnSetStream(c->sol, st);
+    c->dense = dalloc<double>((size_t)n * n);
+    c->piv = dalloc<int>(n);
+    c->dinfo = dalloc<int>(1);
+    if (cusolverDnDgetrf_bufferSize(c->sol, n, n, c->dense, n, &c->lwork) != CUSOLVER_STATUS_SUCCESS)
+      throw Err(LPFEM_ECUDA, "cusolverDnDgetrf_bufferSize");
+    c->dwork = dalloc<double>(std::max(1, c->lwork));
+  }
   for (int i = 0; i < 4; ++i) {
     CK(cudaEventCreate(&c->ev[i]));
     CK(cudaEventCreate(&c->ek[i]));
@@ -1235,7 +1283,8 @@ void lpfem_destroy(lpfem_ctx* c) {
     if (c->cu[s]) cudaFree(c->cu[s]);
     if (c->cp[s]) cudaFree(c->cp[s]);
   }
-  void* ptrs[] = {c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
+  if (c->sol) cusolverDnDestroy(c->sol);
+  void* ptrs[] = {c->dense, c->dwork, c->piv, c->dinfo, c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
                   c->comp_p, c->kmult, c->ref};
   for (void* p : ptrs)
     if (p) cudaFree(p);
