@@ -172,7 +172,7 @@ struct ConduitPrepArgs {
   int np_glob[3];         // P2 nodes per axis of the level's conduit region
   long long n2_glob;      // P2 nodes of the level's conduit region (component stride)
   int porous_gamma_g;     // half-grid index of Gamma in the porous region at the coarse level x R
-  int mode;               // 0 fine composite (B), 1 fine subdomain (A), 2 coarse Picard
+  int mode;               // 0 fine composite (B), 1 fine subdomain (A), 2 coarse Picard, 3 operator only (U)
   double t;
 };
 
@@ -202,6 +202,15 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
     for (int a = 0; a < D; ++a) {
       const long long k = o + a * S.n2 + r;
       double b, lg;
+      if (A.mode == 3) {
+        b = prolong_p2<D>(A.cu_new + a * n2H, A.nHc, A.R, g);
+        base[k] = b;
+        W[k] = b;
+        z[k] = b;
+        lag[k] = 0.0;
+        f[k] = 0.0;
+        continue;
+      }
       if (A.mode == 2) {
         const long long gi = lex<D>(g, A.np_glob);
         b = A.cu_new[a * A.n2_glob + gi];
@@ -218,7 +227,7 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
       f[k] = fv[a];
     }
     double pf = 0.0;
-    if (g[D - 1] == L.G.gamma_g) {
+    if (A.mode != 3 && g[D - 1] == L.G.gamma_g) {
       int gp[3] = {g[0], g[1], g[2]};
       gp[D - 1] = A.porous_gamma_g;
       pf = prolong_p2<D>(A.cpF_old, A.nHp, A.R, gp);
@@ -230,7 +239,9 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
     unlex<D>(k1, shp1, l);
     for (int a = 0; a < D; ++a) g[a] = 2 * (S.c0[a] + l[a]);
     double b;
-    if (A.mode == 2) {
+    if (A.mode == 3) {
+      b = 0.0;
+    } else if (A.mode == 2) {
       int v[3];
       for (int a = 0; a < D; ++a) v[a] = g[a] / 2;
       const int shpg1[3] = {(A.np_glob[0] + 1) / 2, (A.np_glob[1] + 1) / 2, (A.np_glob[2] + 1) / 2};

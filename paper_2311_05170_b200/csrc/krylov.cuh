@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "mlprec.cuh"
 
 namespace lp {
 namespace cgx = cooperative_groups;
@@ -228,8 +229,74 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
 }
 
 // ---------------------------------------------------------------------------------------------
-template <int NT, int TPR, int M>
-__global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A) {
+// M^-1 v for the conduit systems (mlprec.cuh): fine diagonal + nested levels + exact coarse-box solve.
+// v and Z are system-local fine vectors; work is spread over the whole cluster (gt, gs).
+template <int D>
+__device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ v, double* __restrict__ Z, int r0,
+                           int r1, int nrows) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int gt = (int)cl.block_rank() * blockDim.x + threadIdx.x;
+  const int gs = (int)cl.num_blocks() * blockDim.x;
+  SysDesc SF = P.fsys[sid];
+  const double* src = v;
+  double* part = P.part + P.poff[sid];
+  for (int l = 0; l < P.nl; ++l) {
+    const SysDesc SC = P.lsys[l][sid];
+    int ncell = 1;
+    for (int a = 0; a < D; ++a) ncell *= SC.nc[a];
+    for (int it = gt; it < ncell * (D + 1); it += gs) restrict_pass1<D>(SF, SC, P.q[l], src, part, it);
+    cl.sync();
+    double* dst = P.LR[l] + SC.row_off;
+    for (int it = gt; it < SC.nrows; it += gs) restrict_pass2<D>(SC, part, dst, it);
+    cl.sync();
+    src = dst;
+    SF = SC;
+  }
+  if (P.nl > 0) {
+    // exact coarse-box solve: LZ_L = A_L^-1 LR_L (column-major inverse)
+    const SysDesc SC = P.lsys[P.nl - 1][sid];
+    const int n = SC.nrows;
+    const double* Ai = P.aci + P.aoff[sid];
+    const double* rc = P.LR[P.nl - 1] + SC.row_off;
+    double* zc = P.LZ[P.nl - 1] + SC.row_off;
+    for (int i = gt; i < n; i += gs) {
+      double s = 0.0;
+      for (int j = 0; j < n; ++j) s += Ai[(long long)j * n + i] * rc[j];
+      zc[i] = s;
+    }
+    cl.sync();
+    for (int l = P.nl - 2; l >= 0; --l) {
+      const SysDesc SL = P.lsys[l][sid];
+      const SysDesc SU = P.lsys[l + 1][sid];
+      const double* rl = P.LR[l] + SL.row_off;
+      const double* sl = P.LS[l] + SL.row_off;
+      const double* zu = P.LZ[l + 1] + SU.row_off;
+      double* zl = P.LZ[l] + SL.row_off;
+      for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i] + prolong_row<D>(SL, SU, P.q[l + 1], zu, i);
+      cl.sync();
+    }
+  }
+  const SysDesc S0 = P.fsys[sid];
+  const double* s0 = P.s0 + S0.row_off;
+  const double* z1 = P.nl > 0 ? P.LZ[0] + P.lsys[0][sid].row_off : nullptr;
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double si = s0[i];
+    double zi = 0.0;
+    if (si != 0.0) {
+      zi = si * v[i];
+      if (P.nl > 0) zi += prolong_row<D>(S0, P.lsys[0][sid], P.q[0], z1, i);
+    }
+    Z[i] = zi;
+  }
+  (void)nrows;
+}
+
+// ---------------------------------------------------------------------------------------------
+// PC = false: right preconditioning folded into the matrix (A' = mask A diag(s)); the solution is y with
+//             x = s y (applied at write-back).
+// PC = true:  A is the masked unscaled operator and M^-1 = apply_prec; the solution is x itself.
+template <int NT, int TPR, int M, int D, bool PC>
+__global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int CL = (int)cl.num_blocks();
   const int crank = (int)cl.block_rank();
@@ -244,6 +311,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A) {
   double* x = A.x + K.row_off;
   double* r = A.r + K.row_off;
   double* W = A.p + K.row_off;
+  double* Zw = PC ? A.q + K.row_off : nullptr;
   const long long ld = A.rows_total;
   double* V = A.V + K.row_off;
   __shared__ RedSmem<NT, M + 1> S;
@@ -275,7 +343,13 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A) {
     int jend = 0;
     for (int j = 0; j < M; ++j) {
       cl.sync();  // V_j complete
-      spmv_rows<NT, TPR>(rp, col, val, V + j * ld, W, r0, r1);
+      if (PC) {
+        apply_prec<D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
+        cl.sync();
+        spmv_rows<NT, TPR>(rp, col, val, Zw, W, r0, r1);
+      } else {
+        spmv_rows<NT, TPR>(rp, col, val, V + j * ld, W, r0, r1);
+      }
       __syncthreads();
       // CGS pass 1: h = V^T W
       double acc[M + 1];
@@ -359,10 +433,21 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A) {
       }
     }
     __syncthreads();
-    for (int i = r0 + tid; i < r1; i += NT) {
-      double s = x[i];
-      for (int k = 0; k < jend; ++k) s += yv[k] * V[k * ld + i];
-      x[i] = s;
+    if (PC) {
+      for (int i = r0 + tid; i < r1; i += NT) {
+        double s = 0.0;
+        for (int k = 0; k < jend; ++k) s += yv[k] * V[k * ld + i];
+        r[i] = s;
+      }
+      cl.sync();
+      apply_prec<D>(P, sid, r, Zw, r0, r1, K.nrows);
+      for (int i = r0 + tid; i < r1; i += NT) x[i] += Zw[i];
+    } else {
+      for (int i = r0 + tid; i < r1; i += NT) {
+        double s = x[i];
+        for (int k = 0; k < jend; ++k) s += yv[k] * V[k * ld + i];
+        x[i] = s;
+      }
     }
     cl.sync();
     ++nspmv;

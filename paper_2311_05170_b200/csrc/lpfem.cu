@@ -72,7 +72,7 @@ struct Family {
   // porous
   double *val = nullptr, *diag = nullptr, *isq = nullptr, *wn = nullptr;
   // conduit
-  double *aconst = nullptr, *aout = nullptr, *scale = nullptr;
+  double *aconst = nullptr, *aout = nullptr, *scale = nullptr, *mask = nullptr;
   // vectors
   double *base = nullptr, *z = nullptr, *lag = nullptr, *qf = nullptr, *aux = nullptr, *W = nullptr;
   double *rhs = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *V = nullptr, *ecorr = nullptr;
@@ -85,7 +85,7 @@ struct Family {
   std::vector<int> sub_region, sub_pos;  // per local subdomain (fine)
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
-    void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, aconst, aout, scale, base, z, lag, qf, aux, W,
+    void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
                     rhs, x, r, p, q, V, ecorr, dk, dstat};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
@@ -128,6 +128,16 @@ struct lpfem_ctx {
   long long nstep = 0;
   double cur_dt = -1.0;
   double schur_c = 1.0;
+  // multilevel preconditioner of the fine conduit systems (mlprec.cuh)
+  int nl = 0;
+  Level Llv[NLMAX];
+  Family lvl[NLMAX];
+  MLArgs ml{};
+  double *part = nullptr, *aci = nullptr, *abuf = nullptr, *lwk = nullptr;
+  long long *dpoff = nullptr, *daoff = nullptr;
+  std::vector<long long> haoff;
+  int *lpiv = nullptr, *linfo = nullptr;
+  int llwork = 0;
   // coarse Navier-Stokes: dense LU on the device (cuSOLVER), Step 1 dependency (C11)
   cusolverDnHandle_t sol = nullptr;
   double *dense = nullptr, *dwork = nullptr;
@@ -264,7 +274,7 @@ void build_pattern(lpfem_ctx* c, Family& F) {
   CKL();
 }
 
-void alloc_vectors(lpfem_ctx* c, Family& F) {
+void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
   const long long nv = F.kind == 0 ? 3 * F.rows : F.rows;
   F.base = dalloc<double>(nv);
   F.z = dalloc<double>(nv);
@@ -286,9 +296,12 @@ void alloc_vectors(lpfem_ctx* c, Family& F) {
     F.aconst = dalloc<double>(F.nnz);
     F.aout = dalloc<double>(F.nnz);
     F.scale = dalloc<double>(F.rows);
+    F.mask = dalloc<double>(F.rows);
     F.W = dalloc<double>(F.rows);
-    F.V = dalloc<double>((size_t)(GM + 1) * F.rows);
+    F.q = dalloc<double>(F.rows);
+    if (!level_family) F.V = dalloc<double>((size_t)(GM + 1) * F.rows);
   }
+  if (level_family) return;
   if (F.level == 1 && c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN) {
     F.ecorr = dalloc<double>(nv);
     CK(cudaMemsetAsync(F.ecorr, 0, nv * sizeof(double), c->st));
@@ -432,8 +445,8 @@ __global__ void k_picard_norms(const double* u, const double* w, long long n, do
   }
 }
 
-template <class Kern>
-void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const KArgs& a) {
+template <class Kern, class... Args>
+void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Args&... a) {
   if (nsys == 0) return;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nsys * CL);
@@ -447,7 +460,7 @@ void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const KAr
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, k, a));
+  CK(cudaLaunchKernelEx(&cfg, k, a...));
   ++tl_launches;
 }
 
@@ -490,6 +503,23 @@ const RefT<D>* refp(const lpfem_ctx* c) {
 int nHv(const lpfem_ctx* c, int a) { return c->nc_p[a]; }
 
 template <int D>
+void conduit_const(lpfem_ctx* c, Family& C, const Level& L, double dt) {
+  const int nc = (int)C.hs.size();
+  if (!nc) return;
+  cudaStream_t st = c->st;
+  double hmin = 1e300;
+  for (int a = 0; a < D; ++a) hmin = std::min(hmin, L.G.hc[a]);
+  const ConduitCoefs cc = conduit_coefs<D>(c, dt, hmin);
+  k_conduit_const<D><<<grid_rows(C.maxrows, nc), 128, 0, st>>>(C.ds, L, cc, c->kmult, c->nc_p[0], c->nc_p[1],
+                                                                c->nc_p[2], refp<D>(c), C.rowptr, C.col, C.aconst);
+  CKL();
+  k_conduit_scale<D><<<grid_rows(C.maxrows, nc), 128, 0, st>>>(C.ds, L, cc, C.rowptr, C.col, C.aconst, C.scale);
+  CKL();
+  k_mask_from_scale<<<(unsigned)((C.rows + 255) / 256), 256, 0, st>>>(C.scale, C.mask, C.rows);
+  CKL();
+}
+
+template <int D>
 void assemble_dt(lpfem_ctx* c, double dt) {
   cudaStream_t st = c->st;
   const PorousCoefs pc = porous_coefs<D>(c, dt);
@@ -507,21 +537,9 @@ void assemble_dt(lpfem_ctx* c, double dt) {
                                                                    P.rows);
       CKL();
     }
-    Family& C = c->fam[lev][1];
-    const int nc = (int)C.hs.size();
-    if (nc) {
-      double hmin = 1e300;
-      for (int a = 0; a < D; ++a) hmin = std::min(hmin, c->Lc[lev].G.hc[a]);
-      const ConduitCoefs cc = conduit_coefs<D>(c, dt, hmin);
-      k_conduit_const<D><<<grid_rows(C.maxrows, nc), 128, 0, st>>>(C.ds, c->Lc[lev], cc, c->kmult, c->nc_p[0],
-                                                                    c->nc_p[1], c->nc_p[2], refp<D>(c), C.rowptr,
-                                                                    C.col, C.aconst);
-      CKL();
-      k_conduit_scale<D><<<grid_rows(C.maxrows, nc), 128, 0, st>>>(C.ds, c->Lc[lev], cc, C.rowptr, C.col, C.aconst,
-                                                                    C.scale);
-      CKL();
-    }
+    conduit_const<D>(c, c->fam[lev][1], c->Lc[lev], dt);
   }
+  for (int l = 0; l < c->nl; ++l) conduit_const<D>(c, c->lvl[l], c->Llv[l], dt);
   c->cur_dt = dt;
 }
 
@@ -564,10 +582,19 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.rtol = c->opts.krylov_rtol;
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
-  if (D == 2)
-    launch_cluster(k_gmres<512, 8, GM>, (int)C.hk.size(), C.cluster, 512, c->st, a);
-  else
-    launch_cluster(k_gmres<512, 16, GM>, (int)C.hk.size(), C.cluster, 512, c->st, a);
+  a.q = C.q;
+  const bool pc = C.level == 1 && c->nl > 0;
+  if (pc) {
+    if (D == 2)
+      launch_cluster(k_gmres<512, 8, GM, 2, true>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+    else
+      launch_cluster(k_gmres<512, 16, GM, 3, true>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+  } else {
+    if (D == 2)
+      launch_cluster(k_gmres<512, 8, GM, 2, false>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+    else
+      launch_cluster(k_gmres<512, 16, GM, 3, false>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+  }
 }
 
 void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres, bool& ok) {
@@ -643,6 +670,51 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
   CKL();
 }
 
+// Newton-linearised operator of every coarse box (level L of the multilevel preconditioner), inverted densely.
+template <int D>
+void coarse_box_inverses(lpfem_ctx* c, const double* cu_new) {
+  Family& F = c->lvl[c->nl - 1];
+  const Level& L = c->Llv[c->nl - 1];
+  const int ns = (int)F.hs.size();
+  cudaStream_t st = c->st;
+  ConduitPrepArgs A{};
+  A.cu_new = cu_new;
+  for (int a = 0; a < 3; ++a) {
+    A.nHc[a] = c->nc_c[a];
+    A.nHp[a] = c->nc_p[a];
+    A.np_glob[a] = 2 * L.G.n[a] + 1;
+  }
+  A.R = L.G.R;
+  A.mode = 3;
+  k_conduit_prep<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, L, c->pd, c->co, A, F.base, F.z, F.W, F.lag,
+                                                               F.qf, F.aux);
+  CKL();
+  double hmin = 1e300;
+  for (int a = 0; a < D; ++a) hmin = std::min(hmin, L.G.hc[a]);
+  const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
+  k_conduit_step<D><<<grid_rows(F.maxrows, ns), 128, 0, st>>>(F.ds, L, cc, 1, c->kmult, c->nc_p[0], c->nc_p[1],
+                                                               c->nc_p[2], refp<D>(c), F.rowptr, F.col, F.aconst,
+                                                               F.mask, F.z, F.W, F.lag, F.qf, F.aux, F.aout, F.rhs);
+  CKL();
+  const long long tot = c->haoff.back();
+  CK(cudaMemsetAsync(c->abuf, 0, tot * sizeof(double), st));
+  k_dense_batched<<<grid_rows(F.maxrows, ns), 128, 0, st>>>(F.ds, F.rowptr, F.col, F.aout, F.mask, c->daoff, c->abuf);
+  CKL();
+  k_set_identity<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, c->daoff, c->aci);
+  CKL();
+  for (int s2 = 0; s2 < ns; ++s2) {
+    const int n = F.hs[s2].nrows;
+    double* As = c->abuf + c->haoff[s2];
+    double* Bs = c->aci + c->haoff[s2];
+    if (cusolverDnDgetrf(c->sol, n, n, As, n, c->lwk, c->lpiv, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+      throw Err(LPFEM_ECUDA, "cusolverDnDgetrf (coarse box)");
+    if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, As, n, c->lpiv, Bs, n, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+      throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (coarse box)");
+  }
+  k_zero_fixed_inv<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, c->aci);
+  CKL();
+}
+
 template <int D>
 void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, const double* cp_new,
                         const double* cu_old, const double* cpF_old, double* out_u, double* out_p) {
@@ -673,9 +745,12 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   double hmin = 1e300;
   for (int a = 0; a < D; ++a) hmin = std::min(hmin, c->Lc[lev].G.hc[a]);
   const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
+  const bool ml = lev == 1 && c->nl > 0;
+  if (ml) coarse_box_inverses<D>(c, cu_new);
+  double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   k_conduit_step<D><<<grid_rows(C.maxrows, ns), 128, 0, st>>>(C.ds, c->Lc[lev], cc, lev == 1 ? 1 : 0, c->kmult,
                                                                c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), C.rowptr,
-                                                               C.col, C.aconst, C.scale, C.z, C.W, C.lag, C.qf, C.aux,
+                                                               C.col, C.aconst, colscale, C.z, C.W, C.lag, C.qf, C.aux,
                                                                C.aout, C.rhs);
   CKL();
   if (lev == 0) {
@@ -699,7 +774,7 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
     if (lev == 1) CK(cudaEventRecord(c->ek[3], st));
   }
   const int* npg = A.np_glob;
-  k_conduit_writeback<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(C.ds, c->Lc[lev], C.z, C.x, C.scale, C.base,
+  k_conduit_writeback<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(C.ds, c->Lc[lev], C.z, C.x, colscale, C.base,
                                                                     C.ecorr, out_u, out_p, npg[0], npg[1], npg[2],
                                                                     A.n2_glob);
   CKL();
@@ -881,14 +956,101 @@ void setup(lpfem_ctx* c) {
       build_pattern<D>(c, F);
       alloc_vectors(c, F);
     }
+  // multilevel preconditioner of the fine conduit systems: nested levels r h (r = 2, 4, .. dividing R)
+  // and the coarse box at H (mlprec.cuh).  Requires the boxes to lie on coarse grid lines.
+  {
+    Family& FC = c->fam[1][1];
+    bool aligned = !FC.hs.empty();
+    for (auto& S : FC.hs)
+      for (int a = 0; a < D; ++a) aligned = aligned && S.c0[a] % c->R == 0 && S.nc[a] % c->R == 0;
+    std::vector<int> rs;
+    for (int r = 2; r < c->R; r *= 2)
+      if (c->R % r == 0) rs.push_back(r);
+    rs.push_back(c->R);
+    if (aligned && (int)rs.size() <= NLMAX) {
+      c->nl = (int)rs.size();
+      std::vector<long long> poff, aoff;
+      long long ptot = 0, atot = 0;
+      std::vector<long long> pmax(FC.hs.size(), 0);
+      for (int l = 0; l < c->nl; ++l) {
+        const int r = rs[l];
+        Level& L = c->Llv[l];
+        L.G = make_level(D, g.conduit_lo, g.conduit_hi, 1, c->h * r, c->R / r);
+        for (int a = 0; a < 3; ++a) {
+          L.m[a] = a < D ? c->m[a] : 1;
+          L.core[a] = L.G.n[a] / std::max(1, L.m[a]);
+        }
+        Family& F = c->lvl[l];
+        F.kind = 1;
+        F.level = 1;
+        for (size_t si = 0; si < FC.hs.size(); ++si) {
+          SysDesc S = FC.hs[si];
+          S.n2 = 1;
+          S.n1 = 1;
+          for (int a = 0; a < D; ++a) {
+            S.c0[a] /= r;
+            S.nc[a] /= r;
+            S.np[a] = 2 * S.nc[a] + 1;
+            S.n2 *= S.np[a];
+            S.n1 *= S.nc[a] + 1;
+          }
+          S.nrows = D * S.n2 + S.n1;
+          F.hs.push_back(S);
+          long long cells = 1;
+          for (int a = 0; a < D; ++a) cells *= S.nc[a];
+          pmax[si] = std::max(pmax[si], cells * (D + 1) * p3_of(D));
+        }
+        finish_family(D, F);
+        build_pattern<D>(c, F);
+        alloc_vectors(c, F, true);
+        c->ml.q[l] = l == 0 ? r : r / rs[l - 1];
+        c->ml.lsys[l] = F.ds;
+        c->ml.LR[l] = F.r;
+        c->ml.LZ[l] = F.p;
+        c->ml.LS[l] = F.scale;
+      }
+      for (size_t si = 0; si < FC.hs.size(); ++si) {
+        poff.push_back(ptot);
+        ptot += pmax[si];
+        aoff.push_back(atot);
+        const long long n = c->lvl[c->nl - 1].hs[si].nrows;
+        atot += n * n;
+      }
+      aoff.push_back(atot);
+      c->haoff = aoff;
+      c->part = dalloc<double>(ptot);
+      c->aci = dalloc<double>(atot);
+      c->abuf = dalloc<double>(atot);
+      c->dpoff = dalloc<long long>(poff.size());
+      c->daoff = dalloc<long long>(aoff.size());
+      CK(cudaMemcpy(c->dpoff, poff.data(), poff.size() * sizeof(long long), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->daoff, aoff.data(), aoff.size() * sizeof(long long), cudaMemcpyHostToDevice));
+      int nmax = 1;
+      for (auto& S : c->lvl[c->nl - 1].hs) nmax = std::max(nmax, S.nrows);
+      c->lpiv = dalloc<int>(nmax);
+      c->linfo = dalloc<int>(1);
+      c->ml.nl = c->nl;
+      c->ml.part = c->part;
+      c->ml.poff = c->dpoff;
+      c->ml.aci = c->aci;
+      c->ml.aoff = c->daoff;
+      c->ml.fsys = FC.ds;
+      c->ml.s0 = FC.scale;
+    }
+  }
   // cluster sizes: spread the systems of a family over the SMs (deterministic in the global layout)
   {
     int nsm = 148;
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, c->dist.device) == cudaSuccess) nsm = prop.multiProcessorCount;
-    (void)nsm;
     for (int lev = 0; lev < 2; ++lev)
-      for (int k = 0; k < 2; ++k) c->fam[lev][k].cluster = 1;
+      for (int k = 0; k < 2; ++k) {
+        Family& F = c->fam[lev][k];
+        const int nsys = std::max<int>(1, (int)F.hk.size());
+        int cl = 1;
+        while (cl < 8 && nsys * cl * 2 <= nsm) cl *= 2;
+        F.cluster = cl;
+      }
   }
   // states
   for (int s = 0; s < 2; ++s) {
@@ -936,6 +1098,13 @@ void setup(lpfem_ctx* c) {
     if (cusolverDnDgetrf_bufferSize(c->sol, n, n, c->dense, n, &c->lwork) != CUSOLVER_STATUS_SUCCESS)
       throw Err(LPFEM_ECUDA, "cusolverDnDgetrf_bufferSize");
     c->dwork = dalloc<double>(std::max(1, c->lwork));
+    if (c->nl > 0) {
+      int nmax = 1;
+      for (auto& S : c->lvl[c->nl - 1].hs) nmax = std::max(nmax, S.nrows);
+      if (cusolverDnDgetrf_bufferSize(c->sol, nmax, nmax, c->abuf, nmax, &c->llwork) != CUSOLVER_STATUS_SUCCESS)
+        throw Err(LPFEM_ECUDA, "cusolverDnDgetrf_bufferSize");
+      c->lwk = dalloc<double>(std::max(1, c->llwork));
+    }
   }
   for (int i = 0; i < 4; ++i) {
     CK(cudaEventCreate(&c->ev[i]));
@@ -1282,6 +1451,12 @@ void lpfem_destroy(lpfem_ctx* c) {
       if (c->cst[s][f]) cudaFree(c->cst[s][f]);
     if (c->cu[s]) cudaFree(c->cu[s]);
     if (c->cp[s]) cudaFree(c->cp[s]);
+  }
+  for (int l = 0; l < NLMAX; ++l) c->lvl[l].free_all();
+  {
+    void* mp[] = {c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo};
+    for (void* p : mp)
+      if (p) cudaFree(p);
   }
   if (c->sol) cusolverDnDestroy(c->sol);
   void* ptrs[] = {c->dense, c->dwork, c->piv, c->dinfo, c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
