@@ -239,15 +239,10 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
   const int gs = (int)cl.num_blocks() * blockDim.x;
   SysDesc SF = P.fsys[sid];
   const double* src = v;
-  double* part = P.part + P.poff[sid];
   for (int l = 0; l < P.nl; ++l) {
     const SysDesc SC = P.lsys[l][sid];
-    int ncell = 1;
-    for (int a = 0; a < D; ++a) ncell *= SC.nc[a];
-    for (int it = gt; it < ncell * (D + 1); it += gs) restrict_pass1<D>(SF, SC, P.q[l], src, part, it);
-    cl.sync();
     double* dst = P.LR[l] + SC.row_off;
-    for (int it = gt; it < SC.nrows; it += gs) restrict_pass2<D>(SC, part, dst, it);
+    for (int it = gt; it < SC.nrows; it += gs) dst[it] = restrict_row<D>(SF, SC, P.st[l], src, it);
     cl.sync();
     src = dst;
     SF = SC;
@@ -256,13 +251,15 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     // exact coarse-box solve: LZ_L = A_L^-1 LR_L (column-major inverse)
     const SysDesc SC = P.lsys[P.nl - 1][sid];
     const int n = SC.nrows;
-    const double* Ai = P.aci + P.aoff[sid];
+    const double* Ai = P.aci + P.aoff[sid];  // row-major
     const double* rc = P.LR[P.nl - 1] + SC.row_off;
     double* zc = P.LZ[P.nl - 1] + SC.row_off;
-    for (int i = gt; i < n; i += gs) {
+    const int lane = threadIdx.x & 31;
+    for (int i = gt >> 5; i < n; i += gs >> 5) {
       double s = 0.0;
-      for (int j = 0; j < n; ++j) s += Ai[(long long)j * n + i] * rc[j];
-      zc[i] = s;
+      for (int j = lane; j < n; j += 32) s += Ai[(long long)i * n + j] * rc[j];
+      s = warp_sum(s);
+      if (lane == 0) zc[i] = s;
     }
     cl.sync();
     for (int l = P.nl - 2; l >= 0; --l) {

@@ -138,6 +138,7 @@ struct lpfem_ctx {
   std::vector<long long> haoff;
   int *lpiv = nullptr, *linfo = nullptr;
   int llwork = 0;
+  std::vector<void*> stencils;
   // coarse Navier-Stokes: dense LU on the device (cuSOLVER), Step 1 dependency (C11)
   cusolverDnHandle_t sol = nullptr;
   double *dense = nullptr, *dwork = nullptr;
@@ -332,6 +333,75 @@ void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
   CK(cudaMemcpyAsync(F.dk, F.hk.data(), F.hk.size() * sizeof(KSys), cudaMemcpyHostToDevice, c->st));
   F.dstat = dalloc<KStat>(F.hk.size());
   F.hstat.resize(F.hk.size());
+}
+
+// Restriction stencils for ratio q: weights phi_I(x_g) of an interior coarse node I of each parity class at
+// the fine half-grid points g = q l + delta (exact rationals, rounded once).
+template <int D>
+void build_stencil(int q, Stencil& T) {
+  std::memset(&T, 0, sizeof(T));
+  T.q = q;
+  KuhnTables kt;
+  build_kuhn(D, kt);
+  int n = 0;
+  for (int cls = 0; cls < 9; ++cls) {
+    if (cls >= (1 << D) && cls != 8) continue;
+    T.start[cls] = n;
+    int l[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) l[a] = cls == 8 ? 8 : 8 + ((cls >> a) & 1);
+    int rng = 2 * q;
+    int d[3];
+    for (d[2] = (D > 2 ? -rng : 0); d[2] <= (D > 2 ? rng : 0); ++d[2])
+      for (d[1] = -rng; d[1] <= rng; ++d[1])
+        for (d[0] = -rng; d[0] <= rng; ++d[0]) {
+          if (cls == 8 && ((d[0] & 1) || (d[1] & 1) || (d[2] & 1))) continue;
+          int g[3] = {0, 0, 0};
+          for (int a = 0; a < D; ++a) g[a] = q * l[a] + d[a];
+          // coarse simplex containing g: cell, numerators, order (as in the prolongation)
+          int cell[3], num[3], ord[3] = {0, 1, 2};
+          for (int a = 0; a < D; ++a) {
+            cell[a] = g[a] / (2 * q);
+            num[a] = g[a] - 2 * q * cell[a];
+          }
+          std::stable_sort(ord, ord + D, [&](int x, int y) { return num[x] > num[y]; });
+          long long lam[4];
+          lam[0] = 2 * q - num[ord[0]];
+          for (int k = 1; k < D; ++k) lam[k] = num[ord[k - 1]] - num[ord[k]];
+          lam[D] = num[ord[D - 1]];
+          int V[4][3] = {};
+          for (int a = 0; a < D; ++a) V[0][a] = 2 * cell[a];
+          for (int k = 1; k <= D; ++k) {
+            for (int a = 0; a < D; ++a) V[k][a] = V[k - 1][a];
+            V[k][ord[k - 1]] += 2;
+          }
+          double w = 0.0;
+          auto same = [&](const int* P) {
+            for (int a = 0; a < D; ++a)
+              if (P[a] != l[a]) return false;
+            return true;
+          };
+          if (cls == 8) {
+            for (int k = 0; k <= D; ++k)
+              if (same(V[k])) w = (double)lam[k] / (2.0 * q);
+          } else {
+            for (int k = 0; k <= D; ++k)
+              if (same(V[k])) w = (double)(lam[k] * (lam[k] - q)) / (2.0 * q * q);
+            for (int a = 0; a <= D; ++a)
+              for (int b = a + 1; b <= D; ++b) {
+                int E[3];
+                for (int e = 0; e < D; ++e) E[e] = (V[a][e] + V[b][e]) / 2;
+                if (same(E)) w = (double)(2 * lam[a] * lam[b]) / (2.0 * q * q);
+              }
+          }
+          if (w != 0.0) {
+            if (n >= STMAX) throw Err(LPFEM_EINVAL, "restriction stencil table overflow");
+            for (int a = 0; a < 3; ++a) T.off[n][a] = (signed char)(a < D ? d[a] : 0);
+            T.w[n] = w;
+            ++n;
+          }
+        }
+    T.len[cls] = n - T.start[cls];
+  }
 }
 
 // one system = the whole region on the coarse level
@@ -711,7 +781,7 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new) {
     if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, As, n, c->lpiv, Bs, n, c->linfo) != CUSOLVER_STATUS_SUCCESS)
       throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (coarse box)");
   }
-  k_zero_fixed_inv<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, c->aci);
+  k_inv_rowmajor<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, c->aci, c->abuf);
   CKL();
 }
 
@@ -1004,6 +1074,15 @@ void setup(lpfem_ctx* c) {
         build_pattern<D>(c, F);
         alloc_vectors(c, F, true);
         c->ml.q[l] = l == 0 ? r : r / rs[l - 1];
+        {
+          Stencil* hst = new Stencil();
+          build_stencil<D>(c->ml.q[l], *hst);
+          Stencil* dst = dalloc<Stencil>(1);
+          CK(cudaMemcpy(dst, hst, sizeof(Stencil), cudaMemcpyHostToDevice));
+          delete hst;
+          c->stencils.push_back(dst);
+          c->ml.st[l] = dst;
+        }
         c->ml.lsys[l] = F.ds;
         c->ml.LR[l] = F.r;
         c->ml.LZ[l] = F.p;
@@ -1030,9 +1109,7 @@ void setup(lpfem_ctx* c) {
       c->lpiv = dalloc<int>(nmax);
       c->linfo = dalloc<int>(1);
       c->ml.nl = c->nl;
-      c->ml.part = c->part;
-      c->ml.poff = c->dpoff;
-      c->ml.aci = c->aci;
+      c->ml.aci = c->abuf;  // row-major inverses (k_inv_rowmajor)
       c->ml.aoff = c->daoff;
       c->ml.fsys = FC.ds;
       c->ml.s0 = FC.scale;
@@ -1453,6 +1530,7 @@ void lpfem_destroy(lpfem_ctx* c) {
     if (c->cp[s]) cudaFree(c->cp[s]);
   }
   for (int l = 0; l < NLMAX; ++l) c->lvl[l].free_all();
+  for (void* p : c->stencils) cudaFree(p);
   {
     void* mp[] = {c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo};
     for (void* p : mp)

@@ -8,7 +8,7 @@
 // box with its full Newton-linearised operator inverted exactly (dense).  Because the meshes are nested and
 // every form is integrated exactly, the re-discretised level operators equal the Galerkin products
 // P_l^T A P_l (P:443-444 nesting).  P_l are the exact nodal prolongations (P2 velocity, P1 pressure)
-// applied level by level; P_l^T is applied in two deterministic passes (per coarse cell, then per node).
+// applied level by level; P_l^T is a stencil gather per coarse node (weights phi_I(x_g), Stencil).
 // Fixed DOFs (dir / art velocity nodes, art pressure vertices; C4, C5) have zero scaling on every level.
 #pragma once
 #include "assembly.cuh"
@@ -24,12 +24,23 @@ struct MLArgs {
   double* LR[NLMAX];            // restricted vectors (level row space)
   double* LZ[NLMAX];            // level corrections
   const double* LS[NLMAX];      // level scalings (0 on fixed rows)
-  double* part;                 // restriction partials, per system at poff[sid]
-  const long long* poff;
-  const double* aci;            // dense inverses of the coarse-level systems (column-major), at aoff[sid]
+  const double* aci;            // dense inverses of the coarse-level systems (row-major), at aoff[sid]
   const long long* aoff;
   const SysDesc* fsys;          // fine boxes
   const double* s0;             // fine scaling (0 on fixed rows)
+  const struct Stencil* st[NLMAX];  // restriction stencils per level (ratio q[l])
+};
+
+// Restriction P^T as a gather: the weight of coarse node I at fine point g is phi_I(x_g), so P^T v at a
+// coarse node l is sum_delta phi(delta) v[q l + delta] over the fixed stencil of l's parity class, clipped at
+// the box (points outside the box do not exist; the basis function values are cell-independent).
+constexpr int STMAX = 24000;
+struct Stencil {
+  int q;
+  int len[9];      // classes 0..2^D-1 (P2 nodes by half-grid parity), class 8 = P1 vertices
+  int start[9];
+  signed char off[STMAX][3];
+  double w[STMAX];
 };
 
 // P2 prolongation weights of a point g (box-local half-grid of the finer level) in the coarser level box
@@ -58,20 +69,20 @@ __device__ __forceinline__ void p2_weights(const int g[3], int q, const int nc[3
     for (int a = 0; a < D; ++a) V[k][a] = V[k - 1][a];
     V[k][ord[k - 1]] += 2;
   }
-  const double den = 2.0 * (double)q * (double)q;
+  const double inv = 1.0 / (2.0 * (double)q * (double)q);
   int n = 0;
   for (int k = 0; k <= D; ++k, ++n) {
     int c = 0, s = 1;
     for (int a = 0; a < D; ++a, s *= 3) c += V[k][a] * s;
     code[n] = c;
-    w[n] = (double)(lam[k] * (lam[k] - q)) / den;
+    w[n] = (double)(lam[k] * (lam[k] - q)) * inv;
   }
   for (int a = 0; a <= D; ++a)
     for (int b = a + 1; b <= D; ++b, ++n) {
       int c = 0, s = 1;
       for (int e = 0; e < D; ++e, s *= 3) c += ((V[a][e] + V[b][e]) / 2) * s;
       code[n] = c;
-      w[n] = (double)(2 * lam[a] * lam[b]) / den;
+      w[n] = (double)(2 * lam[a] * lam[b]) * inv;
     }
 }
 
@@ -94,12 +105,13 @@ __device__ __forceinline__ void p1_weights(const int g[3], int q, const int nc[3
   for (int k = 1; k < D; ++k) lam[k] = num[ord[k - 1]] - num[ord[k]];
   lam[D] = num[ord[D - 1]];
   int V[3] = {0, 0, 0};
+  const double inv = 1.0 / (2.0 * q);
   for (int k = 0; k <= D; ++k) {
     if (k > 0) V[ord[k - 1]] += 2;
     int c = 0, s = 1;
     for (int a = 0; a < D; ++a, s *= 3) c += V[a] * s;
     code[k] = c;
-    w[k] = (double)lam[k] / (2.0 * q);
+    w[k] = (double)lam[k] * inv;
   }
 }
 
@@ -112,92 +124,43 @@ __device__ __forceinline__ void code_point(int code, const int cell[3], int l[3]
   }
 }
 
-// restriction pass 1: item = (coarse cell, component); partial sums of P^T src over the fine points the
-// prolongation assigns to that cell.
+// restriction by stencil gather: row of the coarse box SC from the finer box SF
 template <int D>
-__device__ void restrict_pass1(const SysDesc& SF, const SysDesc& SC, int q, const double* __restrict__ src,
-                               double* __restrict__ part, int item) {
-  constexpr int NCODE = p3_of(D);
-  const int cidx = item / (D + 1), k = item % (D + 1);
-  int c[3] = {0, 0, 0};
-  unlex<D>(cidx, SC.nc, c);
-  double acc[NCODE];
-#pragma unroll
-  for (int i = 0; i < NCODE; ++i) acc[i] = 0.0;
-  int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-  const int step = k < D ? 1 : 2;
-  for (int a = 0; a < D; ++a) {
-    lo[a] = 2 * q * c[a];
-    hi[a] = 2 * q * c[a] + 2 * q - 1 + (c[a] == SC.nc[a] - 1 ? 1 : 0);
-  }
-  const int shp1[3] = {SF.nc[0] + 1, SF.nc[1] + 1, SF.nc[2] + 1};
-  int g[3] = {0, 0, 0};
-  for (g[2] = lo[2]; g[2] <= (D > 2 ? hi[2] : 0); g[2] += step)
-    for (g[1] = lo[1]; g[1] <= hi[1]; g[1] += step)
-      for (g[0] = lo[0]; g[0] <= hi[0]; g[0] += step) {
-        int cell[3];
-        if (k < D) {
-          const double v = src[(long long)k * SF.n2 + lex<D>(g, SF.np)];
-          if (v == 0.0) continue;
-          int code[n2_of(D)];
-          double w[n2_of(D)];
-          p2_weights<D>(g, q, SC.nc, cell, code, w);
-#pragma unroll
-          for (int n = 0; n < n2_of(D); ++n) acc[code[n]] += w[n] * v;
-        } else {
-          int gv[3];
-          for (int a = 0; a < D; ++a) gv[a] = g[a] >> 1;
-          const double v = src[(long long)D * SF.n2 + lex<D>(gv, shp1)];
-          if (v == 0.0) continue;
-          int code[D + 1];
-          double w[D + 1];
-          p1_weights<D>(g, q, SC.nc, cell, code, w);
-#pragma unroll
-          for (int n = 0; n <= D; ++n) acc[code[n]] += w[n] * v;
-        }
-      }
-  double* o = part + (long long)item * NCODE;
-#pragma unroll
-  for (int i = 0; i < NCODE; ++i) o[i] = acc[i];
-}
-
-// restriction pass 2: item = coarse row (velocity node x comp, then pressure vertex): sum the partials of
-// the adjacent cells.
-template <int D>
-__device__ void restrict_pass2(const SysDesc& SC, const double* __restrict__ part, double* __restrict__ dst,
-                               int row) {
-  int l[3] = {0, 0, 0}, k;
+__device__ __forceinline__ double restrict_row(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
+                                               const double* __restrict__ src, int row) {
+  int l[3] = {0, 0, 0};
+  int cls;
+  const double* sv;
+  const int q = T->q;
+  int shp[3];
   if (row < D * SC.n2) {
-    k = row / SC.n2;
+    const int k = row / SC.n2;
     unlex<D>(row % SC.n2, SC.np, l);
+    cls = 0;
+    for (int a = 0; a < D; ++a) cls |= (l[a] & 1) << a;
+    sv = src + (long long)k * SF.n2;
+    for (int a = 0; a < 3; ++a) shp[a] = SF.np[a];
   } else {
-    k = D;
     const int shp1[3] = {SC.nc[0] + 1, SC.nc[1] + 1, SC.nc[2] + 1};
     unlex<D>(row - D * SC.n2, shp1, l);
     for (int a = 0; a < D; ++a) l[a] *= 2;
+    cls = 8;
+    sv = src + (long long)D * SF.n2;
+    for (int a = 0; a < 3; ++a) shp[a] = SF.nc[a] + 1;
   }
-  int cand[3][2], ncand[3] = {1, 1, 1};
-  for (int a = 0; a < D; ++a) {
-    if (l[a] & 1) {
-      cand[a][0] = (l[a] - 1) >> 1;
-    } else {
-      int n = 0;
-      if ((l[a] >> 1) - 1 >= 0) cand[a][n++] = (l[a] >> 1) - 1;
-      if ((l[a] >> 1) < SC.nc[a]) cand[a][n++] = l[a] >> 1;
-      ncand[a] = n;
-    }
-  }
+  const int b = T->start[cls], e = b + T->len[cls];
   double s = 0.0;
-  for (int i2 = 0; i2 < (D > 2 ? ncand[2] : 1); ++i2)
-    for (int i1 = 0; i1 < ncand[1]; ++i1)
-      for (int i0 = 0; i0 < ncand[0]; ++i0) {
-        int c[3] = {cand[0][i0], cand[1][i1], D > 2 ? cand[2][i2] : 0};
-        int code = 0, m = 1;
-        for (int a = 0; a < D; ++a, m *= 3) code += (l[a] - 2 * c[a]) * m;
-        const long long item = lex<D>(c, SC.nc) * (D + 1) + k;
-        s += part[item * p3_of(D) + code];
-      }
-  dst[row] = s;
+  for (int i = b; i < e; ++i) {
+    int g[3];
+    bool ok = true;
+    for (int a = 0; a < D; ++a) {
+      g[a] = q * l[a] + T->off[i][a];
+      ok = ok && g[a] >= 0 && g[a] <= 2 * SF.nc[a];
+      if (cls == 8) g[a] >>= 1;
+    }
+    if (ok) s += T->w[i] * sv[lex<D>(g, shp)];
+  }
+  return s;
 }
 
 // prolongation of a coarser-level vector src (box SC) to row `row` of the finer level box SF (ratio q)
@@ -266,17 +229,19 @@ __global__ void k_dense_batched(const SysDesc* __restrict__ sys, const long long
     As[(long long)col[q] * n + r] = val[q];
 }
 
-// zero the rows and columns of fixed DOFs in the inverses (column-major)
-__global__ void k_zero_fixed_inv(const SysDesc* __restrict__ sys, const double* __restrict__ mask,
-                                 const long long* __restrict__ aoff, double* __restrict__ A) {
+// row-major copy of the column-major inverses with the rows and columns of fixed DOFs zeroed
+__global__ void k_inv_rowmajor(const SysDesc* __restrict__ sys, const double* __restrict__ mask,
+                               const long long* __restrict__ aoff, const double* __restrict__ Acm,
+                               double* __restrict__ Arm) {
   const SysDesc S = sys[blockIdx.y];
-  int j = blockIdx.x;  // column
-  if (j >= S.nrows) return;
+  int i = blockIdx.x;  // row
+  if (i >= S.nrows) return;
   const int n = S.nrows;
-  double* As = A + aoff[blockIdx.y] + (long long)j * n;
-  const bool fj = mask[S.row_off + j] == 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-    if (fj || mask[S.row_off + i] == 0.0) As[i] = 0.0;
+  const double* src = Acm + aoff[blockIdx.y];
+  double* dst = Arm + aoff[blockIdx.y] + (long long)i * n;
+  const bool fi = mask[S.row_off + i] == 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x)
+    dst[j] = (fi || mask[S.row_off + j] == 0.0) ? 0.0 : src[(long long)j * n + i];
 }
 
 __global__ void k_set_identity(const SysDesc* __restrict__ sys, const long long* __restrict__ aoff,
