@@ -174,12 +174,22 @@ def main():
     if world > 1:
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
-    from paper_2311_05170_b200 import LPFEM, build
-    build.build()
+    from paper_2311_05170_b200 import LPFEM, build, nccl_unique_id
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
     cfg = I.config(args.config)
     D = I.fine_dofs(cfg)
     stream = torch.cuda.Stream()
-    sim = LPFEM(cfg, rank=rank, world=world, device=local, stream=stream.cuda_stream)
+    nid = None
+    if world > 1:
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nid = bytes(t.cpu().numpy().tobytes())
+    sim = LPFEM(cfg, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nid)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     for _ in range(args.warmup):
         sim.step()
@@ -250,7 +260,13 @@ def main():
     if not args.no_e2e:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sim2 = LPFEM(cfg, rank=rank, world=world, device=local, stream=stream.cuda_stream)
+        if world > 1:
+            t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(t, 0)
+            nid = bytes(t.cpu().numpy().tobytes())
+        sim2 = LPFEM(cfg, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nid)
         d2h = 0
         for i in range(args.steps):
             sim2.step()

@@ -159,6 +159,15 @@ lpfem_status lpfem_get_stats(const lpfem_ctx* ctx, lpfem_stats* out);
 lpfem_status lpfem_get_system(lpfem_ctx* ctx, int family, int local_index, int field, long long* nrows,
                               long long* nnz, long long* rowptr, int* col, double* val, double* rhs, double* x);
 
+/* Multi-GPU plan (host only, no device needed): subdomain positions are split into contiguous
+ * blocks over `world` ranks; a fine node belongs to the rank of its owning subdomain (C3).  For one region
+ * meshed with n_cells fine cells per axis, returns global node indices (P2 half-grid lexicographic, or P1
+ * vertex lexicographic if vertex_only): kind 0 = nodes owned by `peer` that `rank` reads (its halo),
+ * 1 = nodes owned by `rank` that `peer` reads, 2 = all nodes owned by `peer`.  Sorted, unique.  out may be
+ * NULL to query the count. */
+lpfem_status lpfem_halo_plan(int dim, const int n_cells[3], const int subdomain_grid[3], int overlap_cells, int rank,
+                             int world, int vertex_only, int kind, int peer, int* out, long long* n_out);
+
 const char* lpfem_last_error(const lpfem_ctx* ctx);
 const char* lpfem_status_string(lpfem_status s);
 void lpfem_destroy(lpfem_ctx* ctx);

@@ -29,7 +29,7 @@ STATUS = ["ok", "einval", "enotdiv", "emisalign", "enoconv", "ecuda", "enccl", "
 # Exported symbols (kept in sync with include/lpfem.h; checked by tests/test_abi.py)
 SYMBOLS = ["lpfem_nccl_unique_id", "lpfem_create", "lpfem_step", "lpfem_get_sizes", "lpfem_get_fields",
            "lpfem_get_coarse_fields", "lpfem_get_mesh", "lpfem_get_layout", "lpfem_get_stats", "lpfem_get_system",
-           "lpfem_last_error", "lpfem_status_string", "lpfem_destroy"]
+           "lpfem_halo_plan", "lpfem_last_error", "lpfem_status_string", "lpfem_destroy"]
 
 
 class Geometry(C.Structure):
@@ -101,6 +101,8 @@ def lib() -> C.CDLL:
         L.lpfem_status_string.restype = C.c_char_p
         L.lpfem_destroy.argtypes = [C.c_void_p]
         L.lpfem_nccl_unique_id.argtypes = [C.c_void_p]
+        L.lpfem_halo_plan.argtypes = [C.c_int, P(C.c_int), P(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.c_int, C.c_void_p, P(C.c_longlong)]
         _LIB = L
     return _LIB
 
@@ -252,3 +254,19 @@ def nccl_unique_id() -> bytes:
     if st != 0:
         raise LPFEMError(st, "ncclGetUniqueId failed")
     return bytes(buf)
+
+
+def halo_plan(dim: int, n_cells, grid, overlap_cells: int, rank: int, world: int, kind: str, peer: int,
+              vertex_only: bool = False) -> np.ndarray:
+    """Host-side multi-GPU plan (lpfem_halo_plan): kind "need" | "give" | "owned"."""
+    L = lib()
+    k = {"need": 0, "give": 1, "owned": 2}[kind]
+    nc = (C.c_int * 3)(*(list(n_cells) + [1] * (3 - dim)))
+    gr = (C.c_int * 3)(*(list(grid) + [1] * (3 - dim)))
+    n = C.c_longlong()
+    st = L.lpfem_halo_plan(dim, nc, gr, overlap_cells, rank, world, int(vertex_only), k, peer, None, C.byref(n))
+    if st != 0:
+        raise LPFEMError(st, "lpfem_halo_plan")
+    out = np.empty(n.value, np.int32)
+    L.lpfem_halo_plan(dim, nc, gr, overlap_cells, rank, world, int(vertex_only), k, peer, _ptr(out), C.byref(n))
+    return out

@@ -17,6 +17,7 @@
 
 #include <cub/device/device_scan.cuh>
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include "../../include/lpfem.h"
 #include "assembly.cuh"
@@ -24,6 +25,7 @@
 #include "krylov.cuh"
 #include "problem.cuh"
 #include "tables.h"
+#include "halo.h"
 
 using namespace lp;
 
@@ -59,6 +61,49 @@ T* dalloc(size_t n) {
 }
 
 constexpr int GM = 30;  // GMRES restart length (compile-time register blocking)
+
+// NCCL is loaded lazily (multi-GPU only) so that the library has no link-time NCCL dependency; in a torch
+// process this resolves to the NCCL torch already loaded.
+struct NcclApi {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+  bool load() {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    send = (decltype(send))dlsym(h, "ncclSend");
+    recv = (decltype(recv))dlsym(h, "ncclRecv");
+    groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
+    groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    return getUniqueId && commInitRank && commDestroy && send && recv && groupStart && groupEnd && errStr;
+  }
+};
+NcclApi g_nccl;
+
+#define CKN(call)                                                                                  \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess) throw Err(LPFEM_ENCCL, std::string(#call) + ": " + g_nccl.errStr(r_));  \
+  } while (0)
+
+// device copy of one peer's index lists and exchange buffers
+struct PeerX {
+  int peer = -1;
+  int np_give = 0, nc_give = 0, np_need = 0, nc_need = 0;
+  int *give_p = nullptr, *give_c = nullptr, *need_p = nullptr, *need_c = nullptr;
+  double *sbuf = nullptr, *rbuf = nullptr;
+};
 
 struct Family {
   int kind = 0;   // 0 porous (scalar P2, 3 fields), 1 conduit (Taylor-Hood saddle)
@@ -139,6 +184,12 @@ struct lpfem_ctx {
   int *lpiv = nullptr, *linfo = nullptr;
   int llwork = 0;
   std::vector<void*> stencils;
+  // multi-GPU (world > 1): NCCL communicator, halo plan, exchange buffers
+  ncclComm_t comm = nullptr;
+  std::vector<PeerX> peers;
+  HaloPlan plan_p, plan_c2, plan_c1;
+  double* gbuf = nullptr;  // gather buffer (root)
+  long long gbuf_n = 0;
   // coarse Navier-Stokes: dense LU on the device (cuSOLVER), Step 1 dependency (C11)
   cusolverDnHandle_t sol = nullptr;
   double *dense = nullptr, *dwork = nullptr;
@@ -147,6 +198,9 @@ struct lpfem_ctx {
 };
 
 namespace {
+
+void setup_multi(lpfem_ctx* c);
+void halo_exchange(lpfem_ctx* c);
 
 // ------------------------------------------------------------------------------------ host setup
 void upload_tables() {
@@ -893,6 +947,7 @@ void do_step(lpfem_ctx* c, double dt) {
   // ---------------- Steps 3-4: fine corrections + write-back
   porous_stage<D>(c, 1, t, c->cst[1], c->cst[0], c->cu[0] + (D - 1) * c->n2c_c, c->comp);
   conduit_solve_once<D>(c, 1, t, c->cu[1], c->cp[1], c->cu[0], c->cst[0][2], c->comp_u, c->comp_p);
+  halo_exchange(c);  // a11: refresh the overlaps of the lagged fields (C2 mode B), world > 1 only
   CK(cudaEventRecord(c->ev[2], st));
   fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
   fetch_stats(c, c->fam[1][1], 1, false, maxres[1], ok);
@@ -1235,6 +1290,7 @@ void setup(lpfem_ctx* c) {
       CKL();
     }
   }
+  if (c->dist.world > 1) setup_multi(c);
   CK(cudaStreamSynchronize(st));
   for (int k = 0; k < 2; ++k) {
     c->stats.n_systems[k] = (long long)c->fam[1][k].hk.size();
@@ -1243,24 +1299,173 @@ void setup(lpfem_ctx* c) {
   }
 }
 
+// buf[f * n + i] = field_f[idx[i]]
+__global__ void k_pack(const int* __restrict__ idx, int n, const double* f0, const double* f1, const double* f2,
+                       double* __restrict__ buf) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int g = idx[i];
+  buf[i] = f0[g];
+  if (f1) buf[n + i] = f1[g];
+  if (f2) buf[2 * n + i] = f2[g];
+}
+__global__ void k_unpack(const int* __restrict__ idx, int n, double* f0, double* f1, double* f2,
+                         const double* __restrict__ buf) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int g = idx[i];
+  f0[g] = buf[i];
+  if (f1) f1[g] = buf[n + i];
+  if (f2) f2[g] = buf[2 * n + i];
+}
+
+int* upload_ints(const std::vector<int>& v) {
+  int* d = dalloc<int>(std::max<size_t>(1, v.size()));
+  if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+  return d;
+}
+
+RegionGrid region_grid(const lpfem_ctx* c, int reg) {
+  RegionGrid G{};
+  G.d = c->D;
+  for (int a = 0; a < 3; ++a) {
+    G.n[a] = a < c->D ? (reg == 0 ? c->nf_p[a] : c->nf_c[a]) : 1;
+    G.m[a] = a < c->D ? c->m[a] : 1;
+  }
+  G.ov = c->ov;
+  return G;
+}
+
+void setup_multi(lpfem_ctx* c) {
+  if (!g_nccl.load()) throw Err(LPFEM_ENCCL, "cannot load libnccl.so.2");
+  ncclUniqueId id;
+  std::memcpy(&id, c->dist.nccl_id, sizeof(id));
+  CKN(g_nccl.commInitRank(&c->comm, c->dist.world, id, c->dist.rank));
+  const int me = c->dist.rank, W = c->dist.world;
+  plan_region(region_grid(c, 0), me, W, false, c->plan_p);
+  plan_region(region_grid(c, 1), me, W, false, c->plan_c2);
+  plan_region(region_grid(c, 1), me, W, true, c->plan_c1);
+  for (int p = 0; p < W; ++p) {
+    if (p == me) continue;
+    PeerX X;
+    X.peer = p;
+    X.np_give = (int)c->plan_p.give[p].size();
+    X.nc_give = (int)c->plan_c2.give[p].size();
+    X.np_need = (int)c->plan_p.need[p].size();
+    X.nc_need = (int)c->plan_c2.need[p].size();
+    X.give_p = upload_ints(c->plan_p.give[p]);
+    X.give_c = upload_ints(c->plan_c2.give[p]);
+    X.need_p = upload_ints(c->plan_p.need[p]);
+    X.need_c = upload_ints(c->plan_c2.need[p]);
+    X.sbuf = dalloc<double>(3LL * X.np_give + (long long)c->D * X.nc_give + 1);
+    X.rbuf = dalloc<double>(3LL * X.np_need + (long long)c->D * X.nc_need + 1);
+    c->peers.push_back(X);
+  }
+  long long mx = 1;
+  for (int p = 0; p < W; ++p)
+    mx = std::max<long long>(mx, 3LL * c->plan_p.owned[p].size() + (long long)c->D * c->plan_c2.owned[p].size() +
+                                     c->plan_c1.owned[p].size());
+  c->gbuf_n = mx;
+  c->gbuf = dalloc<double>(mx);
+}
+
+// overlap refresh after the write-back: owned values of the lagged fields to every peer that reads them
+void halo_exchange(lpfem_ctx* c) {
+  if (c->dist.world <= 1) return;
+  cudaStream_t st = c->st;
+  const int D = c->D;
+  const long long n2c = c->n2c_f;
+  for (auto& X : c->peers) {
+    if (X.np_give) {
+      k_pack<<<(X.np_give + 255) / 256, 256, 0, st>>>(X.give_p, X.np_give, c->comp[0], c->comp[1], c->comp[2], X.sbuf);
+      CKL();
+    }
+    if (X.nc_give) {
+      k_pack<<<(X.nc_give + 255) / 256, 256, 0, st>>>(X.give_c, X.nc_give, c->comp_u, c->comp_u + n2c,
+                                                      D > 2 ? c->comp_u + 2 * n2c : nullptr, X.sbuf + 3LL * X.np_give);
+      CKL();
+    }
+  }
+  CKN(g_nccl.groupStart());
+  for (auto& X : c->peers) {
+    const size_t ns = 3ULL * X.np_give + (size_t)D * X.nc_give, nr = 3ULL * X.np_need + (size_t)D * X.nc_need;
+    if (ns) CKN(g_nccl.send(X.sbuf, ns, ncclFloat64, X.peer, c->comm, st));
+    if (nr) CKN(g_nccl.recv(X.rbuf, nr, ncclFloat64, X.peer, c->comm, st));
+  }
+  CKN(g_nccl.groupEnd());
+  for (auto& X : c->peers) {
+    if (X.np_need) {
+      k_unpack<<<(X.np_need + 255) / 256, 256, 0, st>>>(X.need_p, X.np_need, c->comp[0], c->comp[1], c->comp[2],
+                                                        X.rbuf);
+      CKL();
+    }
+    if (X.nc_need) {
+      k_unpack<<<(X.nc_need + 255) / 256, 256, 0, st>>>(X.need_c, X.nc_need, c->comp_u, c->comp_u + n2c,
+                                                        D > 2 ? c->comp_u + 2 * n2c : nullptr,
+                                                        X.rbuf + 3LL * X.np_need);
+      CKL();
+    }
+  }
+}
+
+// gather every rank's owned composite values on root (collective)
+void gather_root(lpfem_ctx* c, int root) {
+  if (c->dist.world <= 1) return;
+  cudaStream_t st = c->st;
+  const int D = c->D, me = c->dist.rank;
+  const long long n2c = c->n2c_f;
+  auto lists = [&](int p, int*& ip, int*& ic2, int*& ic1) {
+    ip = upload_ints(c->plan_p.owned[p]);
+    ic2 = upload_ints(c->plan_c2.owned[p]);
+    ic1 = upload_ints(c->plan_c1.owned[p]);
+  };
+  if (me != root) {
+    int *ip, *ic2, *ic1;
+    lists(me, ip, ic2, ic1);
+    const int np = (int)c->plan_p.owned[me].size(), nc2 = (int)c->plan_c2.owned[me].size(),
+              nc1 = (int)c->plan_c1.owned[me].size();
+    if (np) k_pack<<<(np + 255) / 256, 256, 0, st>>>(ip, np, c->comp[0], c->comp[1], c->comp[2], c->gbuf);
+    if (nc2)
+      k_pack<<<(nc2 + 255) / 256, 256, 0, st>>>(ic2, nc2, c->comp_u, c->comp_u + n2c,
+                                                D > 2 ? c->comp_u + 2 * n2c : nullptr, c->gbuf + 3LL * np);
+    if (nc1) k_pack<<<(nc1 + 255) / 256, 256, 0, st>>>(ic1, nc1, c->comp_p, nullptr, nullptr,
+                                                       c->gbuf + 3LL * np + (long long)D * nc2);
+    CKL();
+    const size_t n = 3ULL * np + (size_t)D * nc2 + nc1;
+    CKN(g_nccl.send(c->gbuf, n, ncclFloat64, root, c->comm, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(ip);
+    cudaFree(ic2);
+    cudaFree(ic1);
+  } else {
+    for (int p = 0; p < c->dist.world; ++p) {
+      if (p == root) continue;
+      int *ip, *ic2, *ic1;
+      lists(p, ip, ic2, ic1);
+      const int np = (int)c->plan_p.owned[p].size(), nc2 = (int)c->plan_c2.owned[p].size(),
+                nc1 = (int)c->plan_c1.owned[p].size();
+      const size_t n = 3ULL * np + (size_t)D * nc2 + nc1;
+      CKN(g_nccl.recv(c->gbuf, n, ncclFloat64, p, c->comm, st));
+      if (np) k_unpack<<<(np + 255) / 256, 256, 0, st>>>(ip, np, c->comp[0], c->comp[1], c->comp[2], c->gbuf);
+      if (nc2)
+        k_unpack<<<(nc2 + 255) / 256, 256, 0, st>>>(ic2, nc2, c->comp_u, c->comp_u + n2c,
+                                                    D > 2 ? c->comp_u + 2 * n2c : nullptr, c->gbuf + 3LL * np);
+      if (nc1) k_unpack<<<(nc1 + 255) / 256, 256, 0, st>>>(ic1, nc1, c->comp_p, nullptr, nullptr,
+                                                           c->gbuf + 3LL * np + (long long)D * nc2);
+      CKL();
+      CK(cudaStreamSynchronize(st));
+      cudaFree(ip);
+      cudaFree(ic2);
+      cudaFree(ic1);
+    }
+  }
+}
+
 lpfem_status fail(lpfem_ctx* c, const Err& e) {
   if (c) c->err = e.what();
   return e.code;
 }
 
-// NCCL is loaded lazily (multi-GPU only) so that the library has no link-time NCCL dependency.
-struct NcclApi {
-  void* h = nullptr;
-  int (*getUniqueId)(void*) = nullptr;
-  bool load() {
-    if (h) return true;
-    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return false;
-    getUniqueId = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
-    return getUniqueId != nullptr;
-  }
-};
-NcclApi g_nccl;
 
 }  // namespace
 
@@ -1285,7 +1490,7 @@ const char* lpfem_status_string(lpfem_status s) {
 lpfem_status lpfem_nccl_unique_id(unsigned char out[128]) {
   if (!out) return LPFEM_EINVAL;
   if (!g_nccl.load()) return LPFEM_ENCCL;
-  return g_nccl.getUniqueId(out) == 0 ? LPFEM_OK : LPFEM_ENCCL;
+  return g_nccl.getUniqueId((ncclUniqueId*)out) == ncclSuccess ? LPFEM_OK : LPFEM_ENCCL;
 }
 
 lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs, const lpfem_data* data, double H,
@@ -1337,7 +1542,6 @@ lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs
       c->dist.device = 0;
     }
     if (c->dist.world < 1 || c->dist.rank < 0 || c->dist.rank >= c->dist.world) throw Err(LPFEM_EINVAL, "bad dist");
-    if (c->dist.world > 1) throw Err(LPFEM_EINVAL, "multi-GPU halo exchange not built in this version");
     CK(cudaSetDevice(c->dist.device));
     c->st = (cudaStream_t)c->dist.cuda_stream;
     if (coeffs->k_mult) {
@@ -1393,7 +1597,13 @@ static lpfem_status copy_out(lpfem_ctx* c, double* dst, const double* src, long 
 lpfem_status lpfem_get_fields(lpfem_ctx* c, double* pF, double* pf, double* pm, double* u, double* p, int on_device,
                               int root) {
   if (!c) return LPFEM_EINVAL;
-  (void)root;
+  if (root < 0 || root >= c->dist.world) return LPFEM_EINVAL;
+  try {
+    gather_root(c, root);
+  } catch (const Err& e) {
+    return fail(c, e);
+  }
+  if (c->dist.rank != root) return LPFEM_OK;
   lpfem_status s;
   if ((s = copy_out(c, pF, c->comp[2], c->n2p_f, on_device))) return s;
   if ((s = copy_out(c, pf, c->comp[1], c->n2p_f, on_device))) return s;
@@ -1517,6 +1727,27 @@ lpfem_status lpfem_get_system(lpfem_ctx* c, int family, int local_index, int fie
   return LPFEM_OK;
 }
 
+lpfem_status lpfem_halo_plan(int dim, const int n_cells[3], const int subdomain_grid[3], int overlap_cells, int rank,
+                             int world, int vertex_only, int kind, int peer, int* out, long long* n_out) {
+  if (!n_cells || !subdomain_grid || !n_out || dim < 2 || dim > 3 || world < 1 || rank < 0 || rank >= world ||
+      peer < 0 || peer >= world || kind < 0 || kind > 2)
+    return LPFEM_EINVAL;
+  RegionGrid G{};
+  G.d = dim;
+  for (int a = 0; a < 3; ++a) {
+    G.n[a] = a < dim ? n_cells[a] : 1;
+    G.m[a] = a < dim ? subdomain_grid[a] : 1;
+    if (a < dim && (G.m[a] < 1 || G.n[a] % G.m[a])) return LPFEM_EMISALIGN;
+  }
+  G.ov = overlap_cells;
+  HaloPlan P;
+  plan_region(G, rank, world, vertex_only != 0, P);
+  const std::vector<int>& v = kind == 0 ? P.need[peer] : (kind == 1 ? P.give[peer] : P.owned[peer]);
+  *n_out = (long long)v.size();
+  if (out) std::copy(v.begin(), v.end(), out);
+  return LPFEM_OK;
+}
+
 const char* lpfem_last_error(const lpfem_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
 
 void lpfem_destroy(lpfem_ctx* c) {
@@ -1531,6 +1762,13 @@ void lpfem_destroy(lpfem_ctx* c) {
   }
   for (int l = 0; l < NLMAX; ++l) c->lvl[l].free_all();
   for (void* p : c->stencils) cudaFree(p);
+  for (auto& X : c->peers) {
+    void* xp[] = {X.give_p, X.give_c, X.need_p, X.need_c, X.sbuf, X.rbuf};
+    for (void* p : xp)
+      if (p) cudaFree(p);
+  }
+  if (c->gbuf) cudaFree(c->gbuf);
+  if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   {
     void* mp[] = {c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo};
     for (void* p : mp)
