@@ -100,11 +100,14 @@ __device__ __forceinline__ void put_partial(RedSmem<NT, NV>& S, int k, double v)
   if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5][k] = v;
 }
 
-// y[i] = sum_q val[q] x[col[q]] for rows [r0, r1), TPR lanes per row; returns nothing, writes y
+// y[i] = sum_q val[q] x[col[q]] for rows [r0, r1), TPR lanes per row.  Each lane issues its (col, val) loads
+// in batches of U independent loads before the dependent x gathers, so that enough bytes are in flight per SM
+// to cover the HBM latency (Little's law: ~45 KB per SM at ~1 us).
 template <int NT, int TPR>
 __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, const int* __restrict__ col,
                                           const double* __restrict__ val, const double* __restrict__ x,
                                           double* __restrict__ y, int r0, int r1) {
+  constexpr int U = 8;
   const int lane = threadIdx.x % TPR;
   const int grp = threadIdx.x / TPR;
   constexpr int NG = NT / TPR;
@@ -113,7 +116,19 @@ __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, cons
     double s = 0.0;
     if (r < r1) {
       const long long qb = rp[r], qe = rp[r + 1];
-      for (long long q = qb + lane; q < qe; q += TPR) s += val[q] * x[col[q]];
+      for (long long q0 = qb + lane; q0 < qe; q0 += (long long)TPR * U) {
+        int cc[U];
+        double vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long q = q0 + (long long)u * TPR;
+          const bool in = q < qe;
+          cc[u] = in ? __ldg(col + q) : 0;
+          vv[u] = in ? __ldg(val + q) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += vv[u] * x[cc[u]];
+      }
     }
 #pragma unroll
     for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);

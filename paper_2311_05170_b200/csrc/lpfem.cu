@@ -10,6 +10,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -152,9 +153,16 @@ struct lpfem_ctx {
   Level Lp[2], Lc[2];  // [level] porous, conduit
   Family fam[2][2];    // [level][kind]
   // coarse state [old/new]
-  double* cst[2][3] = {};
-  double* cu[2] = {};
-  double* cp[2] = {};
+  // coarse state ring: slot n % 3 holds t_n (Step 1 runs one step ahead on the side stream st2)
+  double* cst[3][3] = {};
+  double* cu[3] = {};
+  double* cp[3] = {};
+  cudaStream_t st2 = nullptr;  // coarse marching stream (overlaps the fine stage)
+  cudaEvent_t evc[3] = {};
+  long long coarse_n = 0;      // latest coarse time index available
+  double coarse_dt = -1.0;
+  bool overlap = true;
+  cusolverDnHandle_t sol2 = nullptr;
   double *wpic = nullptr, *wpic2 = nullptr, *ppic = nullptr, *ppic2 = nullptr;
   double* nrm = nullptr;  // 2 doubles
   // composite fine fields
@@ -883,9 +891,9 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
     k_csr_to_dense<<<(n + 127) / 128, 128, 0, st>>>(C.rowptr, C.col, C.aout, C.scale, n, c->dense);
     CKL();
     CK(cudaMemcpyAsync(C.x, C.rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (cusolverDnDgetrf(c->sol, n, n, c->dense, n, c->dwork, c->piv, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
+    if (cusolverDnDgetrf(c->sol2, n, n, c->dense, n, c->dwork, c->piv, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
       throw Err(LPFEM_ECUDA, "cusolverDnDgetrf");
-    if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, 1, c->dense, n, c->piv, C.x, n, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
+    if (cusolverDnDgetrs(c->sol2, CUBLAS_OP_N, n, 1, c->dense, n, c->piv, C.x, n, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
       throw Err(LPFEM_ECUDA, "cusolverDnDgetrs");
     KStat ks{};
     ks.iters = 1;
@@ -904,26 +912,33 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   CKL();
 }
 
+struct StreamSwap {  // route the launches of the shared stage functions to another stream
+  lpfem_ctx* c;
+  cudaStream_t old;
+  StreamSwap(lpfem_ctx* cc, cudaStream_t s) : c(cc), old(cc->st) { cc->st = s; }
+  ~StreamSwap() { c->st = old; }
+};
+
+// Step 1: coarse state n -> n+1 (ring slots n % 3 -> (n+1) % 3), Algorithm 1 on T_H, on st2.
 template <int D>
-void do_step(lpfem_ctx* c, double dt) {
-  if (dt != c->cur_dt) assemble_dt<D>(c, dt);
-  cudaStream_t st = c->st;
-  const double t = (double)(c->nstep + 1) * dt;  // C18
-  double maxres[2] = {0, 0};
+void coarse_step(lpfem_ctx* c, long long n, double dt) {
+  StreamSwap sw(c, c->st2);
+  cudaStream_t st = c->st2;
+  const int so = (int)(n % 3), sn = (int)((n + 1) % 3);
+  const double t = (double)(n + 1) * dt;  // C18
   bool ok = true;
-  CK(cudaEventRecord(c->ev[0], st));
-  // ---------------- Step 1: coarse, Algorithm 1 on T_H
-  porous_stage<D>(c, 0, t, c->cst[0], c->cst[0], c->cu[0] + (D - 1) * c->n2c_c, c->cst[1]);
+  CK(cudaEventRecord(c->evc[0], st));
+  porous_stage<D>(c, 0, t, c->cst[so], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->cst[sn]);
   {
     double dummy = 0;
     fetch_stats(c, c->fam[0][0], 0, true, dummy, ok);
   }
   const long long nu = (long long)D * c->n2c_c;
-  CK(cudaMemcpyAsync(c->wpic, c->cu[0], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(c->ppic, c->cp[0], c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->wpic, c->cu[so], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->ppic, c->cp[so], c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
   bool pic_ok = false;
   for (int it = 0; it < c->opts.picard_max; ++it) {
-    conduit_solve_once<D>(c, 0, t, c->wpic, c->ppic, c->cu[0], c->cst[0][2], c->wpic2, c->ppic2);
+    conduit_solve_once<D>(c, 0, t, c->wpic, c->ppic, c->cu[so], c->cst[so][2], c->wpic2, c->ppic2);
     double dummy = 0;
     fetch_stats(c, c->fam[0][1], 1, true, dummy, ok);
     k_picard_norms<<<1, 1024, 0, st>>>(c->wpic2, c->wpic, nu, c->nrm);
@@ -941,18 +956,64 @@ void do_step(lpfem_ctx* c, double dt) {
     }
   }
   if (!pic_ok) throw Err(LPFEM_ENOCONV, "coarse Picard iteration did not converge (C11)");
-  CK(cudaMemcpyAsync(c->cu[1], c->wpic, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(c->cp[1], c->ppic, c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaEventRecord(c->ev[1], st));
+  if (!ok) {
+    std::string m = "a coarse Krylov solve did not converge (C19) at n=" + std::to_string(n) + ":";
+    for (int k = 0; k < 2; ++k)
+      for (auto& st0 : c->fam[0][k].hstat)
+        m += " [" + std::to_string(k) + ": it " + std::to_string(st0.iters) + " conv " + std::to_string(st0.converged) +
+             " res " + std::to_string(st0.relres) + "]";
+    throw Err(LPFEM_ENOCONV, m);
+  }
+  CK(cudaMemcpyAsync(c->cu[sn], c->wpic, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(c->cp[sn], c->ppic, c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(c->evc[1], st));
+  CK(cudaEventSynchronize(c->evc[1]));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->evc[0], c->evc[1]));
+  c->stats.t_coarse_ms += ms;
+  c->coarse_n = n + 1;
+  c->coarse_dt = dt;
+}
+
+template <int D>
+void do_step(lpfem_ctx* c, double dt) {
+  if (dt != c->cur_dt) {
+    CK(cudaStreamSynchronize(c->st2));
+    assemble_dt<D>(c, dt);  // on st; the coarse stream must see the new operators
+    CK(cudaEventRecord(c->ev[3], c->st));
+    CK(cudaStreamWaitEvent(c->st2, c->ev[3], 0));
+    c->coarse_n = -1;  // a precomputed coarse step used the old dt
+  }
+  cudaStream_t st = c->st;
+  const long long n = c->nstep;
+  const double t = (double)(n + 1) * dt;  // C18
+  double maxres[2] = {0, 0};
+  bool ok = true;
+  // ---------------- Step 1: coarse state n+1 (precomputed during the previous step when dt is unchanged)
+  if (c->coarse_n != n + 1 || c->coarse_dt != dt) {
+    c->coarse_n = n;
+    coarse_step<D>(c, n, dt);
+  }
+  CK(cudaEventRecord(c->evc[2], c->st2));
+  CK(cudaStreamWaitEvent(st, c->evc[2], 0));
+  const int so = (int)(n % 3), sn = (int)((n + 1) % 3);
   // ---------------- Steps 3-4: fine corrections + write-back
-  porous_stage<D>(c, 1, t, c->cst[1], c->cst[0], c->cu[0] + (D - 1) * c->n2c_c, c->comp);
-  conduit_solve_once<D>(c, 1, t, c->cu[1], c->cp[1], c->cu[0], c->cst[0][2], c->comp_u, c->comp_p);
+  CK(cudaEventRecord(c->ev[1], st));
+  porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+  conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp_u, c->comp_p);
   halo_exchange(c);  // a11: refresh the overlaps of the lagged fields (C2 mode B), world > 1 only
   CK(cudaEventRecord(c->ev[2], st));
+  // ---------------- Step 1 of the next step, overlapped with this fine stage (reads slot n+1, writes n+2)
+  if (c->overlap && !getenv("LPFEM_NO_OVERLAP")) {
+    try {
+      coarse_step<D>(c, n + 1, dt);
+    } catch (const Err&) {
+      c->coarse_n = n + 1;  // recomputed (and reported) at the next step
+    }
+  }
   fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
   fetch_stats(c, c->fam[1][1], 1, false, maxres[1], ok);
-  float ms0 = 0, ms1 = 0, mk0 = 0, mk1 = 0;
-  CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
+  float ms1 = 0, mk0 = 0, mk1 = 0;
   CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
   if (!c->fam[1][0].hs.empty()) CK(cudaEventElapsedTime(&mk0, c->ek[0], c->ek[1]));
   if (!c->fam[1][1].hs.empty()) CK(cudaEventElapsedTime(&mk1, c->ek[2], c->ek[3]));
@@ -960,13 +1021,9 @@ void do_step(lpfem_ctx* c, double dt) {
   c->stats.t_krylov_ms[1] += mk1;
   c->stats.kernel_launches += tl_launches;
   tl_launches = 0;
-  c->stats.t_coarse_ms += ms0;
   c->stats.t_fine_ms += ms1;
   c->stats.max_rel_residual[0] = maxres[0];
   c->stats.max_rel_residual[1] = maxres[1];
-  for (int f = 0; f < 3; ++f) std::swap(c->cst[0][f], c->cst[1][f]);
-  std::swap(c->cu[0], c->cu[1]);
-  std::swap(c->cp[0], c->cp[1]);
   c->nstep++;
   c->stats.steps = c->nstep;
   if (!ok) throw Err(LPFEM_ENOCONV, "a Krylov solve did not reach the relative residual (C19)");
@@ -1185,7 +1242,7 @@ void setup(lpfem_ctx* c) {
       }
   }
   // states
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < 3; ++s) {
     for (int f = 0; f < 3; ++f) c->cst[s][f] = dalloc<double>(c->n2p_c);
     c->cu[s] = dalloc<double>(D * c->n2c_c);
     c->cp[s] = dalloc<double>(c->n1c_c);
@@ -1224,6 +1281,10 @@ void setup(lpfem_ctx* c) {
     const int n = (int)c->fam[0][1].rows;
     if (cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
     cusolverDnSetStream(c->sol, st);
+    CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evc[i], cudaEventDefault));
+    if (cusolverDnCreate(&c->sol2) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
+    cusolverDnSetStream(c->sol2, c->st2);
     c->dense = dalloc<double>((size_t)n * n);
     c->piv = dalloc<int>(n);
     c->dinfo = dalloc<int>(1);
@@ -1617,11 +1678,13 @@ lpfem_status lpfem_get_fields(lpfem_ctx* c, double* pF, double* pf, double* pm, 
 lpfem_status lpfem_get_coarse_fields(lpfem_ctx* c, double* pF, double* pf, double* pm, double* u, double* p) {
   if (!c) return LPFEM_EINVAL;
   lpfem_status s;
-  if ((s = copy_out(c, pF, c->cst[0][2], c->n2p_c, 0))) return s;
-  if ((s = copy_out(c, pf, c->cst[0][1], c->n2p_c, 0))) return s;
-  if ((s = copy_out(c, pm, c->cst[0][0], c->n2p_c, 0))) return s;
-  if ((s = copy_out(c, u, c->cu[0], c->D * c->n2c_c, 0))) return s;
-  if ((s = copy_out(c, p, c->cp[0], c->n1c_c, 0))) return s;
+  const int k = (int)(c->nstep % 3);
+  if (cudaStreamSynchronize(c->st2) != cudaSuccess) return LPFEM_ECUDA;
+  if ((s = copy_out(c, pF, c->cst[k][2], c->n2p_c, 0))) return s;
+  if ((s = copy_out(c, pf, c->cst[k][1], c->n2p_c, 0))) return s;
+  if ((s = copy_out(c, pm, c->cst[k][0], c->n2p_c, 0))) return s;
+  if ((s = copy_out(c, u, c->cu[k], c->D * c->n2c_c, 0))) return s;
+  if ((s = copy_out(c, p, c->cp[k], c->n1c_c, 0))) return s;
   if (cudaStreamSynchronize(c->st) != cudaSuccess) return LPFEM_ECUDA;
   return LPFEM_OK;
 }
@@ -1754,7 +1817,7 @@ void lpfem_destroy(lpfem_ctx* c) {
   if (!c) return;
   for (int lev = 0; lev < 2; ++lev)
     for (int k = 0; k < 2; ++k) c->fam[lev][k].free_all();
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < 3; ++s) {
     for (int f = 0; f < 3; ++f)
       if (c->cst[s][f]) cudaFree(c->cst[s][f]);
     if (c->cu[s]) cudaFree(c->cu[s]);
@@ -1775,6 +1838,13 @@ void lpfem_destroy(lpfem_ctx* c) {
       if (p) cudaFree(p);
   }
   if (c->sol) cusolverDnDestroy(c->sol);
+  if (c->sol2) cusolverDnDestroy(c->sol2);
+  if (c->st2) {
+    cudaStreamSynchronize(c->st2);
+    cudaStreamDestroy(c->st2);
+  }
+  for (int i = 0; i < 3; ++i)
+    if (c->evc[i]) cudaEventDestroy(c->evc[i]);
   void* ptrs[] = {c->dense, c->dwork, c->piv, c->dinfo, c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
                   c->comp_p, c->kmult, c->ref};
   for (void* p : ptrs)
