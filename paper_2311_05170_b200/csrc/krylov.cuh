@@ -257,7 +257,7 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
   for (int l = 0; l < P.nl; ++l) {
     const SysDesc SC = P.lsys[l][sid];
     double* dst = P.LR[l] + SC.row_off;
-    for (int it = gt; it < SC.nrows; it += gs) dst[it] = restrict_row<D>(SF, SC, P.st[l], src, it);
+    for (int it = gt; it < SC.nrows; it += gs) restrict_item<D>(SF, SC, P.st[l], src, dst, it);
     cl.sync();
     src = dst;
     SF = SC;

@@ -124,43 +124,78 @@ __device__ __forceinline__ void code_point(int code, const int cell[3], int l[3]
   }
 }
 
-// restriction by stencil gather: row of the coarse box SC from the finer box SF
+// restriction by stencil gather.  Items are ordered class-major (component, parity class, node) so that the
+// 32 lanes of a warp walk the same stencil: the table reads are warp-uniform (L1 broadcast) and the loop is
+// unrolled for independent loads.  Returns the coarse row index written.
 template <int D>
-__device__ __forceinline__ double restrict_row(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
-                                               const double* __restrict__ src, int row) {
-  int l[3] = {0, 0, 0};
-  int cls;
+__device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
+                                              const double* __restrict__ src, double* __restrict__ dst, int item) {
+  int l[3] = {0, 0, 0}, cls, row;
   const double* sv;
   const int q = T->q;
   int shp[3];
-  if (row < D * SC.n2) {
-    const int k = row / SC.n2;
-    unlex<D>(row % SC.n2, SC.np, l);
+  const int nvel = D * SC.n2;
+  if (item < nvel) {
+    const int k = item / SC.n2;
+    int rem = item - k * SC.n2;
+    // parity classes in order 0..2^D-1; class kappa has prod_a (nc_a + 1 - kappa_a) nodes
     cls = 0;
-    for (int a = 0; a < D; ++a) cls |= (l[a] & 1) << a;
+    for (; cls < (1 << D); ++cls) {
+      int cnt = 1;
+      for (int a = 0; a < D; ++a) cnt *= SC.nc[a] + 1 - ((cls >> a) & 1);
+      if (rem < cnt) break;
+      rem -= cnt;
+    }
+    int ext[3] = {1, 1, 1};
+    for (int a = 0; a < D; ++a) ext[a] = SC.nc[a] + 1 - ((cls >> a) & 1);
+    int i3[3] = {0, 0, 0};
+    unlex<D>(rem, ext, i3);
+    for (int a = 0; a < D; ++a) l[a] = 2 * i3[a] + ((cls >> a) & 1);
+    row = k * SC.n2 + (int)lex<D>(l, SC.np);
     sv = src + (long long)k * SF.n2;
     for (int a = 0; a < 3; ++a) shp[a] = SF.np[a];
   } else {
     const int shp1[3] = {SC.nc[0] + 1, SC.nc[1] + 1, SC.nc[2] + 1};
-    unlex<D>(row - D * SC.n2, shp1, l);
+    unlex<D>(item - nvel, shp1, l);
+    row = item;
     for (int a = 0; a < D; ++a) l[a] *= 2;
     cls = 8;
     sv = src + (long long)D * SF.n2;
     for (int a = 0; a < 3; ++a) shp[a] = SF.nc[a] + 1;
   }
   const int b = T->start[cls], e = b + T->len[cls];
-  double s = 0.0;
-  for (int i = b; i < e; ++i) {
-    int g[3];
-    bool ok = true;
+  const int sh = cls == 8 ? 1 : 0;
+  int base[3] = {0, 0, 0};
+  for (int a = 0; a < D; ++a) base[a] = q * l[a];
+  double s0 = 0.0, s1 = 0.0;
+  int i = b;
+  for (; i + 1 < e; i += 2) {
+    int g0[3], g1[3];
+    bool ok0 = true, ok1 = true;
     for (int a = 0; a < D; ++a) {
-      g[a] = q * l[a] + T->off[i][a];
-      ok = ok && g[a] >= 0 && g[a] <= 2 * SF.nc[a];
-      if (cls == 8) g[a] >>= 1;
+      g0[a] = base[a] + T->off[i][a];
+      g1[a] = base[a] + T->off[i + 1][a];
+      ok0 = ok0 && g0[a] >= 0 && g0[a] <= 2 * SF.nc[a];
+      ok1 = ok1 && g1[a] >= 0 && g1[a] <= 2 * SF.nc[a];
+      g0[a] >>= sh;
+      g1[a] >>= sh;
     }
-    if (ok) s += T->w[i] * sv[lex<D>(g, shp)];
+    const double v0 = ok0 ? sv[lex<D>(g0, shp)] : 0.0;
+    const double v1 = ok1 ? sv[lex<D>(g1, shp)] : 0.0;
+    s0 += T->w[i] * v0;
+    s1 += T->w[i + 1] * v1;
   }
-  return s;
+  if (i < e) {
+    int g0[3];
+    bool ok0 = true;
+    for (int a = 0; a < D; ++a) {
+      g0[a] = base[a] + T->off[i][a];
+      ok0 = ok0 && g0[a] >= 0 && g0[a] <= 2 * SF.nc[a];
+      g0[a] >>= sh;
+    }
+    if (ok0) s0 += T->w[i] * sv[lex<D>(g0, shp)];
+  }
+  dst[row] = s0 + s1;
 }
 
 // prolongation of a coarser-level vector src (box SC) to row `row` of the finer level box SF (ratio q)

@@ -1,0 +1,34 @@
+"""Summarise an ncu --set full report: key metrics per kernel + top stalled SASS lines."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size",
+        "launch__cluster_dim_x", "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_membar_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__inst_executed.sum", "local_load_bytes", "l1tex__t_bytes_pipe_lsu_mem_local_op_ld.sum"]
+
+
+def main(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, u = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")][:70]
+        out.append(f"== {name}")
+        for k in KEYS:
+            if k in h:
+                i = h.index(k)
+                out.append(f"   {k:75s} {r[i]:>18s} {u[i]}")
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
