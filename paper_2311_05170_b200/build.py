@@ -36,7 +36,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", SRC, "-ldl", "-L/usr/local/cuda/lib64", "-lcusolver",
+    extra = os.environ.get("LPFEM_NVCC_EXTRA", "").split()
+    cmd = [NVCC, *FLAGS, *extra, "-o", OUT + ".tmp", SRC, "-ldl", "-L/usr/local/cuda/lib64", "-lcusolver",
            "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -41,6 +41,23 @@ struct KStat {
   long long spmv; // SpMV passes (iterations + residual checks)
 };
 
+// Optional per-phase timing of the GMRES iterations (build with -DLPFEM_PHASE_TIMERS): cluster rank 0,
+// thread 0 of every system accumulates clock64() deltas per phase into A.phase[sid * 16 + k].
+#ifdef LPFEM_PHASE_TIMERS
+#define PHASE(k)                                                        \
+  do {                                                                  \
+    if (threadIdx.x == 0 && crank == 0) {                               \
+      long long t_ = clock64();                                         \
+      A.phase[sid * 16 + (k)] += t_ - tph;                              \
+      tph = t_;                                                         \
+    }                                                                   \
+  } while (0)
+#else
+#define PHASE(k) \
+  do {           \
+  } while (0)
+#endif
+
 struct KArgs {
   const KSys* sys;
   const long long* rowptr;
@@ -57,6 +74,7 @@ struct KArgs {
   double rtol;
   int maxit;
   KStat* stat;
+  long long* phase;  // LPFEM_PHASE_TIMERS only
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -252,21 +270,35 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
   cgx::cluster_group cl = cgx::this_cluster();
   const int gt = (int)cl.block_rank() * blockDim.x + threadIdx.x;
   const int gs = (int)cl.num_blocks() * blockDim.x;
-  SysDesc SF = P.fsys[sid];
-  const double* src = v;
-  for (int l = 0; l < P.nl; ++l) {
-    const SysDesc SC = P.lsys[l][sid];
-    double* dst = P.LR[l] + SC.row_off;
-    for (int it = gt; it < SC.nrows; it += gs) restrict_item<D>(SF, SC, P.st[l], src, dst, it);
+  const SysDesc S0 = P.fsys[sid];
+  if (P.direct) {
+    // every level restricts the fine vector directly (one phase), coarse solve, one fused fine gather
+    int tot = 0;
+    for (int l = 0; l < P.nl; ++l) tot += P.lsys[l][sid].nrows;
+    for (int it = gt; it < tot; it += gs) {
+      int l = 0, rem = it;
+      while (rem >= P.lsys[l][sid].nrows) rem -= P.lsys[l++][sid].nrows;
+      const SysDesc SC = P.lsys[l][sid];
+      restrict_item<D>(S0, SC, P.st[l], v, P.LR[l] + SC.row_off, rem);
+    }
     cl.sync();
-    src = dst;
-    SF = SC;
+  } else {
+    SysDesc SF = S0;
+    const double* src = v;
+    for (int l = 0; l < P.nl; ++l) {
+      const SysDesc SC = P.lsys[l][sid];
+      double* dst = P.LR[l] + SC.row_off;
+      for (int it = gt; it < SC.nrows; it += gs) restrict_item<D>(SF, SC, P.st[l], src, dst, it);
+      cl.sync();
+      src = dst;
+      SF = SC;
+    }
   }
   if (P.nl > 0) {
-    // exact coarse-box solve: LZ_L = A_L^-1 LR_L (column-major inverse)
+    // exact coarse-box solve: LZ_L = A_L^-1 LR_L (row-major inverse, warp per row)
     const SysDesc SC = P.lsys[P.nl - 1][sid];
     const int n = SC.nrows;
-    const double* Ai = P.aci + P.aoff[sid];  // row-major
+    const double* Ai = P.aci + P.aoff[sid];
     const double* rc = P.LR[P.nl - 1] + SC.row_off;
     double* zc = P.LZ[P.nl - 1] + SC.row_off;
     const int lane = threadIdx.x & 31;
@@ -277,26 +309,37 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
       if (lane == 0) zc[i] = s;
     }
     cl.sync();
-    for (int l = P.nl - 2; l >= 0; --l) {
-      const SysDesc SL = P.lsys[l][sid];
-      const SysDesc SU = P.lsys[l + 1][sid];
-      const double* rl = P.LR[l] + SL.row_off;
-      const double* sl = P.LS[l] + SL.row_off;
-      const double* zu = P.LZ[l + 1] + SU.row_off;
-      double* zl = P.LZ[l] + SL.row_off;
-      for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i] + prolong_row<D>(SL, SU, P.q[l + 1], zu, i);
-      cl.sync();
+    if (!P.direct) {
+      for (int l = P.nl - 2; l >= 0; --l) {
+        const SysDesc SL = P.lsys[l][sid];
+        const SysDesc SU = P.lsys[l + 1][sid];
+        const double* rl = P.LR[l] + SL.row_off;
+        const double* sl = P.LS[l] + SL.row_off;
+        const double* zu = P.LZ[l + 1] + SU.row_off;
+        double* zl = P.LZ[l] + SL.row_off;
+        for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i] + prolong_row<D>(SL, SU, P.q[l + 1], zu, i);
+        cl.sync();
+      }
     }
   }
-  const SysDesc S0 = P.fsys[sid];
   const double* s0 = P.s0 + S0.row_off;
-  const double* z1 = P.nl > 0 ? P.LZ[0] + P.lsys[0][sid].row_off : nullptr;
   for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
     const double si = s0[i];
     double zi = 0.0;
     if (si != 0.0) {
       zi = si * v[i];
-      if (P.nl > 0) zi += prolong_row<D>(S0, P.lsys[0][sid], P.q[0], z1, i);
+      if (P.nl > 0) {
+        if (P.direct) {
+          for (int l = 0; l < P.nl - 1; ++l) {
+            const SysDesc SL = P.lsys[l][sid];
+            zi += prolong_row<D>(S0, SL, P.r[l], P.LR[l] + SL.row_off, i, P.LS[l] + SL.row_off);
+          }
+          const SysDesc SC = P.lsys[P.nl - 1][sid];
+          zi += prolong_row<D>(S0, SC, P.r[P.nl - 1], P.LZ[P.nl - 1] + SC.row_off, i);
+        } else {
+          zi += prolong_row<D>(S0, P.lsys[0][sid], P.q[0], P.LZ[0] + P.lsys[0][sid].row_off, i);
+        }
+      }
     }
     Z[i] = zi;
   }
@@ -304,9 +347,33 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------------------
+// Dot products h_k = sum_i Vt_k[i] w[i] (k < nk) of the rows [r0, r1) into the per-warp partials S.red[.][k0+k],
+// in chunks of 8 basis vectors (8 accumulators in registers; w is re-read once per chunk).
+template <int NT, int NV>
+__device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const double* __restrict__ Vt, long long ld,
+                                             const double* __restrict__ w, int nk, int k0, int r0, int r1) {
+  for (int c0 = 0; c0 < nk; c0 += 8) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int i = r0 + threadIdx.x; i < r1; i += NT) {
+      const double wi = w[i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u < nk) acc[u] += Vt[(c0 + u) * ld + i] * wi;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (c0 + u < nk) put_partial(S, k0 + c0 + u, acc[u]);
+  }
+}
+
 // PC = false: right preconditioning folded into the matrix (A' = mask A diag(s)); the solution is y with
 //             x = s y (applied at write-back).
 // PC = true:  A is the masked unscaled operator and M^-1 = apply_prec; the solution is x itself.
+// Arnoldi: classical Gram-Schmidt with the Kahan-Parlett "twice is enough" test: one pass computes V^T w and
+// ||w||^2; ||w'||^2 = ||w||^2 - ||h||^2 decides whether a second projection is needed (||w'|| < ||w||/sqrt 2).
+// The basis is stored unnormalised (Vt_k) with scales sig_k (v_k = sig_k Vt_k), so normalisation costs no pass.
 template <int NT, int TPR, int M, int D, bool PC>
 __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   cgx::cluster_group cl = cgx::this_cluster();
@@ -326,10 +393,13 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   double* Zw = PC ? A.q + K.row_off : nullptr;
   const long long ld = A.rows_total;
   double* V = A.V + K.row_off;
-  __shared__ RedSmem<NT, M + 1> S;
-  __shared__ double H[M + 1][M], cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1];
+  __shared__ RedSmem<NT, M + 2> S;
+  __shared__ double H[M + 1][M], cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1], sig[M + 1];
   int par = 0;
   const int tid = threadIdx.x;
+#ifdef LPFEM_PHASE_TIMERS
+  long long tph = clock64();
+#endif
 
   double pb = 0.0;
   for (int i = r0 + tid; i < r1; i += NT) {
@@ -347,73 +417,76 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   long long vsum = 0;
   if (bnorm == 0.0) conv = 1;
   while (!conv) {
-    for (int i = r0 + tid; i < r1; i += NT) V[i] = r[i] / beta;
+    for (int i = r0 + tid; i < r1; i += NT) V[i] = r[i];
     if (tid == 0) {
+      sig[0] = 1.0 / beta;
       gv[0] = beta;
       for (int k = 1; k <= M; ++k) gv[k] = 0.0;
     }
     int jend = 0;
     for (int j = 0; j < M; ++j) {
-      cl.sync();  // V_j complete
+      cl.sync();  // Vt_j complete, sig visible (smem written by thread 0 before the barrier)
+      PHASE(0);
+      const double sj = sig[j];
       if (PC) {
         apply_prec<D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
+        PHASE(1);
         spmv_rows<NT, TPR>(rp, col, val, Zw, W, r0, r1);
       } else {
         spmv_rows<NT, TPR>(rp, col, val, V + j * ld, W, r0, r1);
       }
       __syncthreads();
-      // CGS pass 1: h = V^T W
-      double acc[M + 1];
-#pragma unroll
-      for (int k = 0; k <= M; ++k) acc[k] = 0.0;
+      PHASE(2);
+      // w = sj * W;  pass A: h_k = sig_k Vt_k^T w and ||w||^2
+      double pw = 0.0;
       for (int i = r0 + tid; i < r1; i += NT) {
-        const double wi = W[i];
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-          if (k <= j) acc[k] += V[k * ld + i] * wi;
-      }
-#pragma unroll
-      for (int k = 0; k < M; ++k)
-        if (k <= j) put_partial(S, k, acc[k]);
-      cluster_sum(S, j + 1, par);
-      if (tid <= j) hc[tid] = S.fin[tid];
-      __syncthreads();
-      // pass 2: W -= V h; h2 = V^T W
-#pragma unroll
-      for (int k = 0; k <= M; ++k) acc[k] = 0.0;
-      for (int i = r0 + tid; i < r1; i += NT) {
-        double wi = W[i];
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-          if (k <= j) wi -= hc[k] * V[k * ld + i];
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-          if (k <= j) acc[k] += V[k * ld + i] * wi;
+        const double wi = sj * W[i];
         W[i] = wi;
+        pw += wi * wi;
       }
-#pragma unroll
-      for (int k = 0; k < M; ++k)
-        if (k <= j) put_partial(S, k, acc[k]);
-      cluster_sum(S, j + 1, par);
-      // pass 3: W -= V h2; ||W||
+      put_partial(S, j + 1, pw);
+      dots_chunked<NT, M + 2>(S, V, ld, W, j + 1, 0, r0, r1);
+      cluster_sum(S, j + 2, par);
+      if (tid <= j) hc[tid] = S.fin[tid] * sig[tid];
+      const double ww = S.fin[j + 1];
+      __syncthreads();
+      PHASE(3);
+      // pass B: w' = w - sum_k h_k v_k, written as Vt_{j+1}; ||w'||^2
+      double* Vn = V + (j + 1) * ld;
       double pn = 0.0;
       for (int i = r0 + tid; i < r1; i += NT) {
         double wi = W[i];
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-          if (k <= j) wi -= S.fin[k] * V[k * ld + i];
-        W[i] = wi;
+        for (int k = 0; k <= j; ++k) wi -= (hc[k] * sig[k]) * V[k * ld + i];
+        Vn[i] = wi;
         pn += wi * wi;
       }
-      if (tid <= j) hc[tid] += S.fin[tid];
-      __syncthreads();
       put_partial(S, 0, pn);
       cluster_sum(S, 1, par);
-      const double hn = sqrt(S.fin[0]);
-      if (hn > 0.0)
-        for (int i = r0 + tid; i < r1; i += NT) V[(j + 1) * ld + i] = W[i] / hn;
+      double hn2 = S.fin[0];
+      PHASE(4);
+      if (hn2 < 0.5 * ww) {
+        // second projection (CGS2): h2 = V^T w', w'' = w' - V h2
+        __syncthreads();
+        dots_chunked<NT, M + 2>(S, V, ld, Vn, j + 1, 0, r0, r1);
+        cluster_sum(S, j + 1, par);
+        double pn2 = 0.0;
+        for (int i = r0 + tid; i < r1; i += NT) {
+          double wi = Vn[i];
+          for (int k = 0; k <= j; ++k) wi -= (S.fin[k] * sig[k] * sig[k]) * V[k * ld + i];
+          Vn[i] = wi;
+          pn2 += wi * wi;
+        }
+        if (tid <= j) hc[tid] += S.fin[tid] * sig[tid];
+        __syncthreads();
+        put_partial(S, 0, pn2);
+        cluster_sum(S, 1, par);
+        hn2 = S.fin[0];
+      }
+      PHASE(5);
+      const double hn = sqrt(hn2);
       if (tid == 0) {
+        sig[j + 1] = hn > 0.0 ? 1.0 / hn : 0.0;
         for (int k = 0; k <= j; ++k) H[k][j] = hc[k];
         H[j + 1][j] = hn;
         for (int k = 0; k < j; ++k) {
@@ -431,6 +504,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         gv[j] = cs[j] * gv[j];
       }
       __syncthreads();
+      PHASE(6);
       ++it;
       vsum += j + 1;
       jend = j + 1;
@@ -443,6 +517,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         for (int m = k + 1; m < jend; ++m) s -= H[k][m] * yv[m];
         yv[k] = H[k][k] != 0.0 ? s / H[k][k] : 0.0;
       }
+      for (int k = 0; k < jend; ++k) yv[k] *= sig[k];
     }
     __syncthreads();
     if (PC) {

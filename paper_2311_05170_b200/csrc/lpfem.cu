@@ -715,18 +715,42 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
+#ifdef LPFEM_PHASE_TIMERS
+  static long long* ph = nullptr;
+  const int nsys_ph = (int)C.hk.size();
+  if (!ph) ph = dalloc<long long>(16 * 4096);
+  CK(cudaMemsetAsync(ph, 0, 16 * nsys_ph * sizeof(long long), c->st));
+  a.phase = ph;
+#endif
   const bool pc = C.level == 1 && c->nl > 0;
+  constexpr int NTG = 1024;
   if (pc) {
     if (D == 2)
-      launch_cluster(k_gmres<512, 8, GM, 2, true>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+      launch_cluster(k_gmres<NTG, 8, GM, 2, true>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
     else
-      launch_cluster(k_gmres<512, 16, GM, 3, true>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+      launch_cluster(k_gmres<NTG, 16, GM, 3, true>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
   } else {
     if (D == 2)
-      launch_cluster(k_gmres<512, 8, GM, 2, false>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+      launch_cluster(k_gmres<NTG, 8, GM, 2, false>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
     else
-      launch_cluster(k_gmres<512, 16, GM, 3, false>, (int)C.hk.size(), C.cluster, 512, c->st, a, c->ml);
+      launch_cluster(k_gmres<NTG, 16, GM, 3, false>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
   }
+#ifdef LPFEM_PHASE_TIMERS
+  if (C.level == 1) {
+    std::vector<long long> h(16 * nsys_ph);
+    std::vector<KStat> ks(nsys_ph);
+    CK(cudaMemcpyAsync(h.data(), ph, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(ks.data(), C.dstat, ks.size() * sizeof(KStat), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    int worst = 0;
+    for (int i = 0; i < nsys_ph; ++i)
+      if (ks[i].iters > ks[worst].iters) worst = i;
+    fprintf(stderr, "[phases] system %d iters %d, us per iteration:", worst, ks[worst].iters);
+    const char* nm[7] = {"sync/V", "prec", "spmv", "cgs1", "cgs2", "cgs3", "norm+givens"};
+    for (int k = 0; k < 7; ++k) fprintf(stderr, " %s %.2f", nm[k], h[16 * worst + k] / 1965.0 / std::max(1, ks[worst].iters));
+    fprintf(stderr, "\n");
+  }
+#endif
 }
 
 void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres, bool& ok) {
@@ -1186,9 +1210,11 @@ void setup(lpfem_ctx* c) {
         build_pattern<D>(c, F);
         alloc_vectors(c, F, true);
         c->ml.q[l] = l == 0 ? r : r / rs[l - 1];
+        c->ml.r[l] = r;
+        c->ml.direct = getenv("LPFEM_ML_DIRECT") ? 1 : 0;  // experiment: one-phase restriction to all levels
         {
           Stencil* hst = new Stencil();
-          build_stencil<D>(c->ml.q[l], *hst);
+          build_stencil<D>(c->ml.direct ? r : c->ml.q[l], *hst);
           Stencil* dst = dalloc<Stencil>(1);
           CK(cudaMemcpy(dst, hst, sizeof(Stencil), cudaMemcpyHostToDevice));
           delete hst;

@@ -28,7 +28,9 @@ struct MLArgs {
   const long long* aoff;
   const SysDesc* fsys;          // fine boxes
   const double* s0;             // fine scaling (0 on fixed rows)
-  const struct Stencil* st[NLMAX];  // restriction stencils per level (ratio q[l])
+  const struct Stencil* st[NLMAX];  // restriction stencils per level (ratio q[l]; direct mode: ratio r[l])
+  int direct;                   // 1: every level restricts from / prolongs to the fine system directly
+  int r[NLMAX];                 // ratio of level l to the fine mesh
 };
 
 // Restriction P^T as a gather: the weight of coarse node I at fine point g is phi_I(x_g), so P^T v at a
@@ -201,7 +203,8 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
 // prolongation of a coarser-level vector src (box SC) to row `row` of the finer level box SF (ratio q)
 template <int D>
 __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& SC, int q,
-                                              const double* __restrict__ src, int row) {
+                                              const double* __restrict__ src, int row,
+                                              const double* __restrict__ scl = nullptr) {
   int g[3] = {0, 0, 0}, cell[3];
   double s = 0.0;
   if (row < D * SF.n2) {
@@ -210,13 +213,13 @@ __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& 
     int code[n2_of(D)];
     double w[n2_of(D)];
     p2_weights<D>(g, q, SC.nc, cell, code, w);
-    const double* sk = src + (long long)k * SC.n2;
 #pragma unroll
     for (int n = 0; n < n2_of(D); ++n) {
       if (w[n] == 0.0) continue;
       int l[3];
       code_point<D>(code[n], cell, l);
-      s += w[n] * sk[lex<D>(l, SC.np)];
+      const long long id = (long long)k * SC.n2 + lex<D>(l, SC.np);
+      s += w[n] * (scl ? scl[id] * src[id] : src[id]);
     }
   } else {
     const int shpf[3] = {SF.nc[0] + 1, SF.nc[1] + 1, SF.nc[2] + 1};
@@ -226,14 +229,14 @@ __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& 
     double w[D + 1];
     p1_weights<D>(g, q, SC.nc, cell, code, w);
     const int shpc[3] = {SC.nc[0] + 1, SC.nc[1] + 1, SC.nc[2] + 1};
-    const double* sp = src + (long long)D * SC.n2;
 #pragma unroll
     for (int n = 0; n <= D; ++n) {
       if (w[n] == 0.0) continue;
       int l[3];
       code_point<D>(code[n], cell, l);
       for (int a = 0; a < D; ++a) l[a] >>= 1;
-      s += w[n] * sp[lex<D>(l, shpc)];
+      const long long id = (long long)D * SC.n2 + lex<D>(l, shpc);
+      s += w[n] * (scl ? scl[id] * src[id] : src[id]);
     }
   }
   return s;
