@@ -264,6 +264,8 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
 // ---------------------------------------------------------------------------------------------
 // M^-1 v for the conduit systems (mlprec.cuh): fine diagonal + nested levels + exact coarse-box solve.
 // v and Z are system-local fine vectors; work is spread over the whole cluster (gt, gs).
+constexpr int RLN = 8;  // lanes per restricted row
+
 template <int D>
 __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ v, double* __restrict__ Z, int r0,
                            int r1, int nrows) {
@@ -275,11 +277,13 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     // every level restricts the fine vector directly (one phase), coarse solve, one fused fine gather
     int tot = 0;
     for (int l = 0; l < P.nl; ++l) tot += P.lsys[l][sid].nrows;
-    for (int it = gt; it < tot; it += gs) {
-      int l = 0, rem = it;
+    // warp-uniform trip count (the lane groups of a warp shuffle together)
+    const int wfirst = (gt & ~31) / RLN;
+    for (int it = gt / RLN, w0 = wfirst; w0 < tot; it += gs / RLN, w0 += gs / RLN) {
+      int l = 0, rem = it < tot ? it : tot - 1;
       while (rem >= P.lsys[l][sid].nrows) rem -= P.lsys[l++][sid].nrows;
       const SysDesc SC = P.lsys[l][sid];
-      restrict_item<D>(S0, SC, P.st[l], v, P.LR[l] + SC.row_off, rem);
+      restrict_item<D, RLN>(S0, SC, P.st[l], v, P.LR[l] + SC.row_off, it < tot ? rem : SC.nrows, gt % RLN);
     }
     cl.sync();
   } else {
@@ -288,7 +292,9 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     for (int l = 0; l < P.nl; ++l) {
       const SysDesc SC = P.lsys[l][sid];
       double* dst = P.LR[l] + SC.row_off;
-      for (int it = gt; it < SC.nrows; it += gs) restrict_item<D>(SF, SC, P.st[l], src, dst, it);
+      const int wfirst = (gt & ~31) / RLN;  // warp-uniform trip count (shuffles inside)
+      for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN)
+        restrict_item<D, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
       cl.sync();
       src = dst;
       SF = SC;

@@ -126,12 +126,16 @@ __device__ __forceinline__ void code_point(int code, const int cell[3], int l[3]
   }
 }
 
-// restriction by stencil gather.  Items are ordered class-major (component, parity class, node) so that the
-// 32 lanes of a warp walk the same stencil: the table reads are warp-uniform (L1 broadcast) and the loop is
-// unrolled for independent loads.  Returns the coarse row index written.
-template <int D>
+// restriction by stencil gather.  Items are ordered class-major (component, parity class, node) so that
+// neighbouring items walk the same stencil; each item's stencil is split over LN lanes (lane = 0..LN-1 of an
+// aligned lane group) and reduced with shuffles, which cuts the dependent-load chain per row by LN.
+template <int D, int LN>
 __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
-                                              const double* __restrict__ src, double* __restrict__ dst, int item) {
+                                              const double* __restrict__ src, double* __restrict__ dst, int item,
+                                              int lane) {
+  // every lane of the warp must reach the shuffles below: out-of-range items contribute nothing
+  const bool valid = item < SC.nrows;
+  if (!valid) item = 0;
   int l[3] = {0, 0, 0}, cls, row;
   const double* sv;
   const int q = T->q;
@@ -169,25 +173,8 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
   const int sh = cls == 8 ? 1 : 0;
   int base[3] = {0, 0, 0};
   for (int a = 0; a < D; ++a) base[a] = q * l[a];
-  double s0 = 0.0, s1 = 0.0;
-  int i = b;
-  for (; i + 1 < e; i += 2) {
-    int g0[3], g1[3];
-    bool ok0 = true, ok1 = true;
-    for (int a = 0; a < D; ++a) {
-      g0[a] = base[a] + T->off[i][a];
-      g1[a] = base[a] + T->off[i + 1][a];
-      ok0 = ok0 && g0[a] >= 0 && g0[a] <= 2 * SF.nc[a];
-      ok1 = ok1 && g1[a] >= 0 && g1[a] <= 2 * SF.nc[a];
-      g0[a] >>= sh;
-      g1[a] >>= sh;
-    }
-    const double v0 = ok0 ? sv[lex<D>(g0, shp)] : 0.0;
-    const double v1 = ok1 ? sv[lex<D>(g1, shp)] : 0.0;
-    s0 += T->w[i] * v0;
-    s1 += T->w[i + 1] * v1;
-  }
-  if (i < e) {
+  double s0 = 0.0;
+  for (int i = b + lane; valid && i < e; i += LN) {
     int g0[3];
     bool ok0 = true;
     for (int a = 0; a < D; ++a) {
@@ -197,7 +184,9 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
     }
     if (ok0) s0 += T->w[i] * sv[lex<D>(g0, shp)];
   }
-  dst[row] = s0 + s1;
+#pragma unroll
+  for (int o = LN / 2; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o, LN);
+  if (valid && lane == 0) dst[row] = s0;
 }
 
 // prolongation of a coarser-level vector src (box SC) to row `row` of the finer level box SF (ratio q)
