@@ -266,35 +266,38 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
 // v and Z are system-local fine vectors; work is spread over the whole cluster (gt, gs).
 constexpr int RLN = 8;  // lanes per restricted row
 
-template <int D>
+template <int D, int NC>
 __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ v, double* __restrict__ Z, int r0,
                            int r1, int nrows) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int gt = (int)cl.block_rank() * blockDim.x + threadIdx.x;
   const int gs = (int)cl.num_blocks() * blockDim.x;
-  const SysDesc S0 = P.fsys[sid];
+  const int f = sid / P.nsub, bx = sid % P.nsub;
+  const SysDesc S0 = P.fsys[bx];
+  auto LRp = [&](int l) { return P.LR[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
+  auto LZp = [&](int l) { return P.LZ[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
+  auto LSp = [&](int l) { return P.LS[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
   if (P.direct) {
     // every level restricts the fine vector directly (one phase), coarse solve, one fused fine gather
     int tot = 0;
-    for (int l = 0; l < P.nl; ++l) tot += P.lsys[l][sid].nrows;
-    // warp-uniform trip count (the lane groups of a warp shuffle together)
-    const int wfirst = (gt & ~31) / RLN;
+    for (int l = 0; l < P.nl; ++l) tot += P.lsys[l][bx].nrows;
+    const int wfirst = (gt & ~31) / RLN;  // warp-uniform trip count (the lane groups of a warp shuffle together)
     for (int it = gt / RLN, w0 = wfirst; w0 < tot; it += gs / RLN, w0 += gs / RLN) {
       int l = 0, rem = it < tot ? it : tot - 1;
-      while (rem >= P.lsys[l][sid].nrows) rem -= P.lsys[l++][sid].nrows;
-      const SysDesc SC = P.lsys[l][sid];
-      restrict_item<D, RLN>(S0, SC, P.st[l], v, P.LR[l] + SC.row_off, it < tot ? rem : SC.nrows, gt % RLN);
+      while (rem >= P.lsys[l][bx].nrows) rem -= P.lsys[l++][bx].nrows;
+      const SysDesc SC = P.lsys[l][bx];
+      restrict_item<D, NC, RLN>(S0, SC, P.st[l], v, LRp(l), it < tot ? rem : SC.nrows, gt % RLN);
     }
     cl.sync();
   } else {
     SysDesc SF = S0;
     const double* src = v;
     for (int l = 0; l < P.nl; ++l) {
-      const SysDesc SC = P.lsys[l][sid];
-      double* dst = P.LR[l] + SC.row_off;
+      const SysDesc SC = P.lsys[l][bx];
+      double* dst = LRp(l);
       const int wfirst = (gt & ~31) / RLN;  // warp-uniform trip count (shuffles inside)
       for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN)
-        restrict_item<D, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
+        restrict_item<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
       cl.sync();
       src = dst;
       SF = SC;
@@ -302,11 +305,11 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
   }
   if (P.nl > 0) {
     // exact coarse-box solve: LZ_L = A_L^-1 LR_L (row-major inverse, warp per row)
-    const SysDesc SC = P.lsys[P.nl - 1][sid];
+    const SysDesc SC = P.lsys[P.nl - 1][bx];
     const int n = SC.nrows;
     const double* Ai = P.aci + P.aoff[sid];
-    const double* rc = P.LR[P.nl - 1] + SC.row_off;
-    double* zc = P.LZ[P.nl - 1] + SC.row_off;
+    const double* rc = LRp(P.nl - 1);
+    double* zc = LZp(P.nl - 1);
     const int lane = threadIdx.x & 31;
     for (int i = gt >> 5; i < n; i += gs >> 5) {
       double s = 0.0;
@@ -317,18 +320,18 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     cl.sync();
     if (!P.direct) {
       for (int l = P.nl - 2; l >= 0; --l) {
-        const SysDesc SL = P.lsys[l][sid];
-        const SysDesc SU = P.lsys[l + 1][sid];
-        const double* rl = P.LR[l] + SL.row_off;
-        const double* sl = P.LS[l] + SL.row_off;
-        const double* zu = P.LZ[l + 1] + SU.row_off;
-        double* zl = P.LZ[l] + SL.row_off;
-        for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i] + prolong_row<D>(SL, SU, P.q[l + 1], zu, i);
+        const SysDesc SL = P.lsys[l][bx];
+        const SysDesc SU = P.lsys[l + 1][bx];
+        const double* rl = LRp(l);
+        const double* sl = LSp(l);
+        const double* zu = LZp(l + 1);
+        double* zl = LZp(l);
+        for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i] + prolong_row<D, NC>(SL, SU, P.q[l + 1], zu, i);
         cl.sync();
       }
     }
   }
-  const double* s0 = P.s0 + S0.row_off;
+  const double* s0 = P.s0 + f * P.fstride + S0.row_off;
   for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
     const double si = s0[i];
     double zi = 0.0;
@@ -336,20 +339,118 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
       zi = si * v[i];
       if (P.nl > 0) {
         if (P.direct) {
-          for (int l = 0; l < P.nl - 1; ++l) {
-            const SysDesc SL = P.lsys[l][sid];
-            zi += prolong_row<D>(S0, SL, P.r[l], P.LR[l] + SL.row_off, i, P.LS[l] + SL.row_off);
-          }
-          const SysDesc SC = P.lsys[P.nl - 1][sid];
-          zi += prolong_row<D>(S0, SC, P.r[P.nl - 1], P.LZ[P.nl - 1] + SC.row_off, i);
+          for (int l = 0; l < P.nl - 1; ++l)
+            zi += prolong_row<D, NC>(S0, P.lsys[l][bx], P.r[l], LRp(l), i, LSp(l));
+          zi += prolong_row<D, NC>(S0, P.lsys[P.nl - 1][bx], P.r[P.nl - 1], LZp(P.nl - 1), i);
         } else {
-          zi += prolong_row<D>(S0, P.lsys[0][sid], P.q[0], P.LZ[0] + P.lsys[0][sid].row_off, i);
+          zi += prolong_row<D, NC>(S0, P.lsys[0][bx], P.q[0], LZp(0), i);
         }
       }
     }
     Z[i] = zi;
   }
   (void)nrows;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Preconditioned CG with the multilevel preconditioner (porous systems, SPD): unscaled masked operator,
+// z = M^-1 r (symmetric: restriction = transpose of the prolongation), stopping test on the unscaled residual
+// (C19) with the mask as weights.  One cluster per system; x, r, p, q, z are system-local.
+template <int NT, int TPR, int D>
+__global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __restrict__ zbuf) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const int sid = blockIdx.x / CL;
+  const KSys K = A.sys[sid];
+  const int chunk = (K.nrows + CL - 1) / CL;
+  const int r0 = min(K.nrows, crank * chunk), r1 = min(K.nrows, r0 + chunk);
+  const long long* rp = A.rowptr + K.prow_off;
+  const int* col = A.col;
+  const double* val = A.val + K.val_off;
+  const double* b = A.b + K.row_off;
+  const double* w = A.w + K.row_off;
+  double* x = A.x + K.row_off;
+  double* r = A.r + K.row_off;
+  double* p = A.p + K.row_off;
+  double* q = A.q + K.row_off;
+  double* z = zbuf + K.row_off;
+  __shared__ RedSmem<NT, 2> S;
+  int par = 0;
+  const int tid = threadIdx.x;
+  double pw = 0.0;
+  for (int i = r0 + tid; i < r1; i += NT) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    pw += w[i] * bi * bi;
+  }
+  put_partial(S, 0, pw);
+  cluster_sum(S, 1, par);
+  const double bnorm = sqrt(S.fin[0]);
+  const double tol2 = A.rtol * A.rtol * S.fin[0];
+  int it = 0, conv = 0, nspmv = 0, checks = 0;
+  double relres = 0.0, rz = 0.0;
+  bool fresh = true;  // p must be restarted from z
+  if (bnorm == 0.0) conv = 1;
+  while (!conv) {
+    // z = M^-1 r, rz = r . z
+    cl.sync();
+    apply_prec<D, 1>(P, sid, r, z, r0, r1, K.nrows);
+    double prz = 0.0;
+    for (int i = r0 + tid; i < r1; i += NT) prz += r[i] * z[i];
+    put_partial(S, 0, prz);
+    cluster_sum(S, 1, par);
+    const double rzn = S.fin[0];
+    const double beta = fresh ? 0.0 : rzn / rz;
+    rz = rzn;
+    fresh = false;
+    for (int i = r0 + tid; i < r1; i += NT) p[i] = z[i] + beta * p[i];
+    cl.sync();
+    spmv_rows<NT, TPR>(rp, col, val, p, q, r0, r1);
+    __syncthreads();
+    double ppq = 0.0;
+    for (int i = r0 + tid; i < r1; i += NT) ppq += p[i] * q[i];
+    put_partial(S, 0, ppq);
+    cluster_sum(S, 1, par);
+    const double pq = S.fin[0];
+    const double alpha = pq != 0.0 ? rz / pq : 0.0;
+    double prr = 0.0;
+    for (int i = r0 + tid; i < r1; i += NT) {
+      x[i] += alpha * p[i];
+      const double ri = r[i] - alpha * q[i];
+      r[i] = ri;
+      prr += w[i] * ri * ri;
+    }
+    put_partial(S, 0, prr);
+    cluster_sum(S, 1, par);
+    ++it;
+    if (S.fin[0] <= tol2 || it >= A.maxit || pq == 0.0) {
+      ++nspmv;
+      cl.sync();
+      spmv_rows<NT, TPR>(rp, col, val, x, q, r0, r1);
+      __syncthreads();
+      double pt = 0.0;
+      for (int i = r0 + tid; i < r1; i += NT) {
+        const double ri = b[i] - q[i];
+        r[i] = ri;
+        pt += w[i] * ri * ri;
+      }
+      put_partial(S, 0, pt);
+      cluster_sum(S, 1, par);
+      relres = sqrt(S.fin[0]) / bnorm;
+      if (S.fin[0] <= tol2) conv = 1;
+      else if (it >= A.maxit || ++checks > 20 || pq == 0.0) break;
+      else fresh = true;
+    }
+  }
+  if (crank == 0 && tid == 0) {
+    A.stat[sid].iters = it;
+    A.stat[sid].converged = conv;
+    A.stat[sid].relres = relres;
+    A.stat[sid].vsum = 0;
+    A.stat[sid].spmv = it + nspmv;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -435,7 +536,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       PHASE(0);
       const double sj = sig[j];
       if (PC) {
-        apply_prec<D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
+        apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);
         spmv_rows<NT, TPR>(rp, col, val, Zw, W, r0, r1);
@@ -533,7 +634,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         r[i] = s;
       }
       cl.sync();
-      apply_prec<D>(P, sid, r, Zw, r0, r1, K.nrows);
+      apply_prec<D, D>(P, sid, r, Zw, r0, r1, K.nrows);
       for (int i = r0 + tid; i < r1; i += NT) x[i] += Zw[i];
     } else {
       for (int i = r0 + tid; i < r1; i += NT) {

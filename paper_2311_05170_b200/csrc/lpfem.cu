@@ -116,7 +116,7 @@ struct Family {
   long long* rowptr = nullptr;
   int* col = nullptr;
   // porous
-  double *val = nullptr, *diag = nullptr, *isq = nullptr, *wn = nullptr;
+  double *val = nullptr, *diag = nullptr, *isq = nullptr, *wn = nullptr, *dinv = nullptr, *zv = nullptr;
   // conduit
   double *aconst = nullptr, *aout = nullptr, *scale = nullptr, *mask = nullptr;
   // vectors
@@ -131,7 +131,7 @@ struct Family {
   std::vector<int> sub_region, sub_pos;  // per local subdomain (fine)
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
-    void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
+    void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, dinv, zv, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
                     rhs, x, r, p, q, V, ecorr, dk, dstat};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
@@ -192,6 +192,14 @@ struct lpfem_ctx {
   int *lpiv = nullptr, *linfo = nullptr;
   int llwork = 0;
   std::vector<void*> stencils;
+  // multilevel preconditioner of the fine porous PCG (same level ratios, scalar P2)
+  int nlp = 0;
+  Family plv[NLMAX];
+  Level Lplv[NLMAX];
+  MLArgs mlp{};
+  double *aci_p = nullptr, *abuf_p = nullptr;
+  long long* daoff_p = nullptr;
+  std::vector<long long> haoff_p;
   // multi-GPU (world > 1): NCCL communicator, halo plan, exchange buffers
   ncclComm_t comm = nullptr;
   std::vector<PeerX> peers;
@@ -651,6 +659,45 @@ void conduit_const(lpfem_ctx* c, Family& C, const Level& L, double dt) {
   CKL();
 }
 
+// porous multilevel preconditioner: level diagonals and the coarse-box inverses (the porous operators are
+// time-invariant for fixed dt, so this runs once per dt)
+template <int D>
+void porous_levels(lpfem_ctx* c, double dt) {
+  cudaStream_t st = c->st;
+  const PorousCoefs pc = porous_coefs<D>(c, dt);
+  for (int l = 0; l < c->nlp; ++l) {
+    Family& F = c->plv[l];
+    const int ns = (int)F.hs.size();
+    k_porous_assemble<D><<<grid_rows(F.maxrows, ns), 128, 0, st>>>(F.ds, c->Lplv[l], pc, c->kmult, c->nc_p[0],
+                                                                    c->nc_p[1], c->nc_p[2], refp<D>(c), F.rowptr,
+                                                                    F.col, F.val, F.nnz, F.diag, F.rows);
+    CKL();
+    k_porous_invdiag<D><<<grid_rows(F.maxrows, ns), 128, 0, st>>>(F.ds, c->Lplv[l], F.diag, F.dinv, F.wn, F.rows);
+    CKL();
+  }
+  Family& F = c->plv[c->nlp - 1];
+  const int ns = (int)F.hs.size();
+  const long long tot = c->haoff_p.back();
+  CK(cudaMemsetAsync(c->abuf_p, 0, tot * sizeof(double), st));
+  k_dense_porous<<<dim3((F.maxrows + 127) / 128, 3 * ns), 128, 0, st>>>(F.ds, ns, F.rowptr, F.col, F.val, F.nnz, F.wn,
+                                                                      F.rows, c->daoff_p, c->abuf_p);
+  CKL();
+  k_set_identity_n<<<dim3(F.maxrows, 3 * ns), 128, 0, st>>>(F.ds, ns, c->daoff_p, c->aci_p);
+  CKL();
+  for (int sid = 0; sid < 3 * ns; ++sid) {
+    const int n = F.hs[sid % ns].nrows;
+    double* As = c->abuf_p + c->haoff_p[sid];
+    double* Bs = c->aci_p + c->haoff_p[sid];
+    if (cusolverDnDgetrf(c->sol, n, n, As, n, c->lwk, c->lpiv, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+      throw Err(LPFEM_ECUDA, "cusolverDnDgetrf (porous coarse box)");
+    if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, As, n, c->lpiv, Bs, n, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+      throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (porous coarse box)");
+  }
+  k_inv_rowmajor_porous<<<dim3(F.maxrows, 3 * ns), 128, 0, st>>>(F.ds, ns, F.wn, F.rows, c->daoff_p, c->aci_p,
+                                                                 c->abuf_p);
+  CKL();
+}
+
 template <int D>
 void assemble_dt(lpfem_ctx* c, double dt) {
   cudaStream_t st = c->st;
@@ -663,7 +710,12 @@ void assemble_dt(lpfem_ctx* c, double dt) {
           P.ds, c->Lp[lev], pc, c->kmult, c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), P.rowptr, P.col, P.val,
           P.nnz, P.diag, P.rows);
       CKL();
-      k_porous_isq<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, c->Lp[lev], P.diag, P.isq, P.rows);
+      if (lev == 1 && c->nlp > 0) {
+        // multilevel PCG: masked unscaled operator; isq := 0/1 mask, dinv = 1/diag for the fine Jacobi part
+        k_porous_invdiag<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, c->Lp[lev], P.diag, P.dinv, P.isq, P.rows);
+      } else {
+        k_porous_isq<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, c->Lp[lev], P.diag, P.isq, P.rows);
+      }
       CKL();
       k_porous_scale<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, P.rowptr, P.col, P.val, P.nnz, P.isq,
                                                                    P.rows);
@@ -672,6 +724,7 @@ void assemble_dt(lpfem_ctx* c, double dt) {
     conduit_const<D>(c, c->fam[lev][1], c->Lc[lev], dt);
   }
   for (int l = 0; l < c->nl; ++l) conduit_const<D>(c, c->lvl[l], c->Llv[l], dt);
+  if (c->nlp > 0) porous_levels<D>(c, dt);
   c->cur_dt = dt;
 }
 
@@ -692,10 +745,16 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.rtol = c->opts.krylov_rtol;
   a.maxit = c->opts.max_iter;
   a.stat = P.dstat;
-  if (D == 2)
+  if (P.level == 1 && c->nlp > 0) {
+    if (D == 2)
+      launch_cluster(k_pcg_ml<1024, 4, 2>, (int)P.hk.size(), P.cluster, 1024, c->st, a, c->mlp, P.zv);
+    else
+      launch_cluster(k_pcg_ml<1024, 8, 3>, (int)P.hk.size(), P.cluster, 1024, c->st, a, c->mlp, P.zv);
+  } else if (D == 2) {
     launch_cluster(k_cg<1024, 4>, (int)P.hk.size(), P.cluster, 1024, c->st, a);
-  else
+  } else {
     launch_cluster(k_cg<1024, 8>, (int)P.hk.size(), P.cluster, 1024, c->st, a);
+  }
 }
 
 template <int D>
@@ -1244,13 +1303,87 @@ void setup(lpfem_ctx* c) {
       CK(cudaMemcpy(c->daoff, aoff.data(), aoff.size() * sizeof(long long), cudaMemcpyHostToDevice));
       int nmax = 1;
       for (auto& S : c->lvl[c->nl - 1].hs) nmax = std::max(nmax, S.nrows);
-      c->lpiv = dalloc<int>(nmax);
+      c->lpiv = dalloc<int>(nmax + 4096);
       c->linfo = dalloc<int>(1);
       c->ml.nl = c->nl;
       c->ml.aci = c->abuf;  // row-major inverses (k_inv_rowmajor)
       c->ml.aoff = c->daoff;
       c->ml.fsys = FC.ds;
       c->ml.s0 = FC.scale;
+      c->ml.nsub = (int)FC.hs.size();
+      for (int l = 0; l < NLMAX; ++l) c->ml.lstride[l] = 0;
+      c->ml.fstride = 0;
+      // ---- porous: same level ratios on the porous boxes (scalar P2, three fields per box)
+      Family& FP = c->fam[1][0];
+      bool aligned_p = !FP.hs.empty();
+      for (auto& S : FP.hs)
+        for (int a = 0; a < D; ++a) aligned_p = aligned_p && S.c0[a] % c->R == 0 && S.nc[a] % c->R == 0;
+      if (aligned_p && !getenv("LPFEM_NO_POROUS_ML")) {
+        c->nlp = c->nl;
+        std::vector<long long> aoffp;
+        long long atp = 0;
+        for (int l = 0; l < c->nlp; ++l) {
+          const int r = rs[l];
+          Level& L = c->Lplv[l];
+          L.G = make_level(D, g.porous_lo, g.porous_hi, 0, c->h * r, c->R / r);
+          for (int a = 0; a < 3; ++a) {
+            L.m[a] = a < D ? c->m[a] : 1;
+            L.core[a] = L.G.n[a] / std::max(1, L.m[a]);
+          }
+          Family& F = c->plv[l];
+          F.kind = 0;
+          F.level = 1;
+          for (size_t si = 0; si < FP.hs.size(); ++si) {
+            SysDesc S = FP.hs[si];
+            S.n2 = 1;
+            S.n1 = 1;
+            for (int a = 0; a < D; ++a) {
+              S.c0[a] /= r;
+              S.nc[a] /= r;
+              S.np[a] = 2 * S.nc[a] + 1;
+              S.n2 *= S.np[a];
+              S.n1 *= S.nc[a] + 1;
+            }
+            S.nrows = S.n2;
+            F.hs.push_back(S);
+          }
+          finish_family(D, F);
+          build_pattern<D>(c, F);
+          alloc_vectors(c, F, true);
+          F.dinv = dalloc<double>(3 * F.rows);
+          c->mlp.q[l] = c->ml.q[l];
+          c->mlp.r[l] = r;
+          c->mlp.st[l] = c->ml.st[l];
+          c->mlp.lsys[l] = F.ds;
+          c->mlp.LR[l] = F.r;
+          c->mlp.LZ[l] = F.p;
+          c->mlp.LS[l] = F.dinv;
+          c->mlp.lstride[l] = F.rows;
+        }
+        const Family& FL = c->plv[c->nlp - 1];
+        for (int f = 0; f < 3; ++f)
+          for (size_t si = 0; si < FP.hs.size(); ++si) {
+            aoffp.push_back(atp);
+            const long long n = FL.hs[si].nrows;
+            atp += n * n;
+          }
+        aoffp.push_back(atp);
+        c->haoff_p = aoffp;
+        c->aci_p = dalloc<double>(atp);
+        c->abuf_p = dalloc<double>(atp);
+        c->daoff_p = dalloc<long long>(aoffp.size());
+        CK(cudaMemcpy(c->daoff_p, aoffp.data(), aoffp.size() * sizeof(long long), cudaMemcpyHostToDevice));
+        FP.dinv = dalloc<double>(3 * FP.rows);
+        FP.zv = dalloc<double>(3 * FP.rows);
+        c->mlp.nl = c->nlp;
+        c->mlp.direct = 0;
+        c->mlp.nsub = (int)FP.hs.size();
+        c->mlp.aci = c->abuf_p;  // row-major inverses
+        c->mlp.aoff = c->daoff_p;
+        c->mlp.fsys = FP.ds;
+        c->mlp.s0 = FP.dinv;
+        c->mlp.fstride = FP.rows;
+      }
     }
   }
   // cluster sizes: spread the systems of a family over the SMs (deterministic in the global layout)
@@ -1320,6 +1453,8 @@ void setup(lpfem_ctx* c) {
     if (c->nl > 0) {
       int nmax = 1;
       for (auto& S : c->lvl[c->nl - 1].hs) nmax = std::max(nmax, S.nrows);
+      if (c->nlp > 0)
+        for (auto& S : c->plv[c->nlp - 1].hs) nmax = std::max(nmax, S.nrows);
       if (cusolverDnDgetrf_bufferSize(c->sol, nmax, nmax, c->abuf, nmax, &c->llwork) != CUSOLVER_STATUS_SUCCESS)
         throw Err(LPFEM_ECUDA, "cusolverDnDgetrf_bufferSize");
       c->lwk = dalloc<double>(std::max(1, c->llwork));
@@ -1850,6 +1985,12 @@ void lpfem_destroy(lpfem_ctx* c) {
     if (c->cp[s]) cudaFree(c->cp[s]);
   }
   for (int l = 0; l < NLMAX; ++l) c->lvl[l].free_all();
+  for (int l = 0; l < NLMAX; ++l) c->plv[l].free_all();
+  {
+    void* pp[] = {c->aci_p, c->abuf_p, c->daoff_p};
+    for (void* p : pp)
+      if (p) cudaFree(p);
+  }
   for (void* p : c->stencils) cudaFree(p);
   for (auto& X : c->peers) {
     void* xp[] = {X.give_p, X.give_c, X.need_p, X.need_c, X.sbuf, X.rbuf};

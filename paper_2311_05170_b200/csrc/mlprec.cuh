@@ -31,6 +31,9 @@ struct MLArgs {
   const struct Stencil* st[NLMAX];  // restriction stencils per level (ratio q[l]; direct mode: ratio r[l])
   int direct;                   // 1: every level restricts from / prolongs to the fine system directly
   int r[NLMAX];                 // ratio of level l to the fine mesh
+  int nsub;                     // boxes per field: system sid = field * nsub + box
+  long long lstride[NLMAX];     // field stride of the level vectors / scalings
+  long long fstride;            // field stride of the fine scaling s0
 };
 
 // Restriction P^T as a gather: the weight of coarse node I at fine point g is phi_I(x_g), so P^T v at a
@@ -126,10 +129,71 @@ __device__ __forceinline__ void code_point(int code, const int cell[3], int l[3]
   }
 }
 
+// 1/diag on free rows, 0 on fixed rows (level scalings and the fine Jacobi part of the porous preconditioner)
+template <int D>
+__global__ void k_porous_invdiag(const SysDesc* __restrict__ sys, Level L, const double* __restrict__ diag,
+                                 double* __restrict__ dinv, double* __restrict__ mask, long long rows_total) {
+  const SysDesc S = sys[blockIdx.y];
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= S.nrows) return;
+  int l[3] = {0, 0, 0};
+  unlex<D>(r, S.np, l);
+  const bool fixed = node_class<D>(L.G, S, l) >= CL_ART;
+  for (int f = 0; f < 3; ++f) {
+    const long long k = f * rows_total + S.row_off + r;
+    dinv[k] = fixed ? 0.0 : 1.0 / diag[k];
+    if (mask) mask[k] = fixed ? 0.0 : 1.0;
+  }
+}
+
+// dense copies of the porous coarse-box systems, one per (field, box): system sid = field * nsub + box
+__global__ void k_dense_porous(const SysDesc* __restrict__ sys, int nsub, const long long* __restrict__ rowptr,
+                               const int* __restrict__ col, const double* __restrict__ val, long long nnz_total,
+                               const double* __restrict__ mask, long long rows_total,
+                               const long long* __restrict__ aoff, double* __restrict__ A) {
+  const int sid = blockIdx.y, f = sid / nsub, b = sid % nsub;
+  const SysDesc S = sys[b];
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= S.nrows) return;
+  const int n = S.nrows;
+  double* As = A + aoff[sid];
+  if (mask[f * rows_total + S.row_off + r] == 0.0) {
+    As[(long long)r * n + r] = 1.0;
+    return;
+  }
+  for (long long q = rowptr[S.row_off + r]; q < rowptr[S.row_off + r + 1]; ++q)
+    As[(long long)col[q] * n + r] = val[f * nnz_total + q];
+}
+
+__global__ void k_inv_rowmajor_porous(const SysDesc* __restrict__ sys, int nsub, const double* __restrict__ mask,
+                                      long long rows_total, const long long* __restrict__ aoff,
+                                      const double* __restrict__ Acm, double* __restrict__ Arm) {
+  const int sid = blockIdx.y, f = sid / nsub, b = sid % nsub;
+  const SysDesc S = sys[b];
+  int i = blockIdx.x;
+  if (i >= S.nrows) return;
+  const int n = S.nrows;
+  const double* m = mask + f * rows_total + S.row_off;
+  const double* src = Acm + aoff[sid];
+  double* dst = Arm + aoff[sid] + (long long)i * n;
+  const bool fi = m[i] == 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = (fi || m[j] == 0.0) ? 0.0 : src[(long long)j * n + i];
+}
+
+__global__ void k_set_identity_n(const SysDesc* __restrict__ sys, int nsub, const long long* __restrict__ aoff,
+                                 double* __restrict__ B) {
+  const SysDesc S = sys[blockIdx.y % nsub];
+  int j = blockIdx.x;
+  if (j >= S.nrows) return;
+  const int n = S.nrows;
+  double* Bs = B + aoff[blockIdx.y] + (long long)j * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) Bs[i] = i == j ? 1.0 : 0.0;
+}
+
 // restriction by stencil gather.  Items are ordered class-major (component, parity class, node) so that
 // neighbouring items walk the same stencil; each item's stencil is split over LN lanes (lane = 0..LN-1 of an
 // aligned lane group) and reduced with shuffles, which cuts the dependent-load chain per row by LN.
-template <int D, int LN>
+template <int D, int NC, int LN>
 __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
                                               const double* __restrict__ src, double* __restrict__ dst, int item,
                                               int lane) {
@@ -140,7 +204,7 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
   const double* sv;
   const int q = T->q;
   int shp[3];
-  const int nvel = D * SC.n2;
+  const int nvel = NC * SC.n2;
   if (item < nvel) {
     const int k = item / SC.n2;
     int rem = item - k * SC.n2;
@@ -166,7 +230,7 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
     row = item;
     for (int a = 0; a < D; ++a) l[a] *= 2;
     cls = 8;
-    sv = src + (long long)D * SF.n2;
+    sv = src + (long long)NC * SF.n2;
     for (int a = 0; a < 3; ++a) shp[a] = SF.nc[a] + 1;
   }
   const int b = T->start[cls], e = b + T->len[cls];
@@ -190,13 +254,13 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
 }
 
 // prolongation of a coarser-level vector src (box SC) to row `row` of the finer level box SF (ratio q)
-template <int D>
+template <int D, int NC>
 __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& SC, int q,
                                               const double* __restrict__ src, int row,
                                               const double* __restrict__ scl = nullptr) {
   int g[3] = {0, 0, 0}, cell[3];
   double s = 0.0;
-  if (row < D * SF.n2) {
+  if (row < NC * SF.n2) {
     const int k = row / SF.n2;
     unlex<D>(row % SF.n2, SF.np, g);
     int code[n2_of(D)];
@@ -212,7 +276,7 @@ __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& 
     }
   } else {
     const int shpf[3] = {SF.nc[0] + 1, SF.nc[1] + 1, SF.nc[2] + 1};
-    unlex<D>(row - D * SF.n2, shpf, g);
+    unlex<D>(row - NC * SF.n2, shpf, g);
     for (int a = 0; a < D; ++a) g[a] *= 2;
     int code[D + 1];
     double w[D + 1];
@@ -224,7 +288,7 @@ __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& 
       int l[3];
       code_point<D>(code[n], cell, l);
       for (int a = 0; a < D; ++a) l[a] >>= 1;
-      const long long id = (long long)D * SC.n2 + lex<D>(l, shpc);
+      const long long id = (long long)NC * SC.n2 + lex<D>(l, shpc);
       s += w[n] * (scl ? scl[id] * src[id] : src[id]);
     }
   }
