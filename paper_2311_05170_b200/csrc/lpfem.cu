@@ -192,6 +192,7 @@ struct lpfem_ctx {
   int *lpiv = nullptr, *linfo = nullptr;
   int llwork = 0;
   std::vector<void*> stencils;
+  int* gjperm = nullptr;  // pivot scratch of the batched Gauss-Jordan inversion
   // multilevel preconditioner of the fine porous PCG (same level ratios, scalar P2)
   int nlp = 0;
   Family plv[NLMAX];
@@ -915,19 +916,31 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new) {
   CK(cudaMemsetAsync(c->abuf, 0, tot * sizeof(double), st));
   k_dense_batched<<<grid_rows(F.maxrows, ns), 128, 0, st>>>(F.ds, F.rowptr, F.col, F.aout, F.mask, c->daoff, c->abuf);
   CKL();
-  k_set_identity<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, c->daoff, c->aci);
-  CKL();
-  for (int s2 = 0; s2 < ns; ++s2) {
-    const int n = F.hs[s2].nrows;
-    double* As = c->abuf + c->haoff[s2];
-    double* Bs = c->aci + c->haoff[s2];
-    if (cusolverDnDgetrf(c->sol, n, n, As, n, c->lwk, c->lpiv, c->linfo) != CUSOLVER_STATUS_SUCCESS)
-      throw Err(LPFEM_ECUDA, "cusolverDnDgetrf (coarse box)");
-    if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, As, n, c->lpiv, Bs, n, c->linfo) != CUSOLVER_STATUS_SUCCESS)
-      throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (coarse box)");
+  int nmax = 1;
+  for (auto& S2 : F.hs) nmax = std::max(nmax, S2.nrows);
+  if (nmax <= 512) {
+    // small boxes (2D): batched in-place Gauss-Jordan, one CTA per matrix
+    const size_t smem = 2 * (size_t)nmax * sizeof(double);
+    k_gj_inverse<1024><<<ns, 1024, smem, st>>>(F.ds, c->daoff, c->abuf, c->gjperm);
+    CKL();
+    std::swap(c->abuf, c->aci);  // aci: column-major inverses; abuf receives the row-major copy below
+  } else {
+    // large boxes (3D): dense LU per matrix (cuSOLVER), inverse by solving with the identity
+    k_set_identity<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, c->daoff, c->aci);
+    CKL();
+    for (int s2 = 0; s2 < ns; ++s2) {
+      const int n = F.hs[s2].nrows;
+      double* As = c->abuf + c->haoff[s2];
+      double* Bs = c->aci + c->haoff[s2];
+      if (cusolverDnDgetrf(c->sol, n, n, As, n, c->lwk, c->lpiv, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+        throw Err(LPFEM_ECUDA, "cusolverDnDgetrf (coarse box)");
+      if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, As, n, c->lpiv, Bs, n, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+        throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (coarse box)");
+    }
   }
   k_inv_rowmajor<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, c->aci, c->abuf);
   CKL();
+  c->ml.aci = c->abuf;
 }
 
 template <int D>
@@ -1297,6 +1310,7 @@ void setup(lpfem_ctx* c) {
       c->part = dalloc<double>(ptot);
       c->aci = dalloc<double>(atot);
       c->abuf = dalloc<double>(atot);
+      c->gjperm = dalloc<int>(atot);
       c->dpoff = dalloc<long long>(poff.size());
       c->daoff = dalloc<long long>(aoff.size());
       CK(cudaMemcpy(c->dpoff, poff.data(), poff.size() * sizeof(long long), cudaMemcpyHostToDevice));
@@ -2000,7 +2014,7 @@ void lpfem_destroy(lpfem_ctx* c) {
   if (c->gbuf) cudaFree(c->gbuf);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   {
-    void* mp[] = {c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo};
+    void* mp[] = {c->gjperm, c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo};
     for (void* p : mp)
       if (p) cudaFree(p);
   }

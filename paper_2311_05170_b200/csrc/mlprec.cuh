@@ -320,6 +320,103 @@ __global__ void k_dense_batched(const SysDesc* __restrict__ sys, const long long
     As[(long long)col[q] * n + r] = val[q];
 }
 
+// Batched in-place Gauss-Jordan inversion with partial pivoting, one CTA per matrix (column-major, n from
+// the system descriptor).  Per pivot step: argmax reduction over the pivot column, row interchange, then the
+// rank-1 update of all entries from the pivot row/column staged in shared memory.  The row interchanges are
+// undone as column interchanges at the end (classic in-place Gauss-Jordan).  Used for the coarse-box
+// operators of the multilevel preconditioner (n ~ 10^2 - 10^3).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_gj_inverse(const SysDesc* __restrict__ sys, const long long* __restrict__ aoff,
+                                                   double* __restrict__ Aall, int* __restrict__ perm_all) {
+  extern __shared__ double sm[];
+  const SysDesc S = sys[blockIdx.x];
+  const int n = S.nrows;
+  double* A = Aall + aoff[blockIdx.x];
+  int* perm = perm_all + (aoff[blockIdx.x] / 1);  // scratch of length n inside a per-matrix region
+  double* rowk = sm;          // n
+  double* colk = sm + n;      // n
+  __shared__ double rv[NT / 32];
+  __shared__ int ri[NT / 32];
+  __shared__ int piv_s;
+  const int tid = threadIdx.x;
+  for (int k = 0; k < n; ++k) {
+    // pivot search in column k, rows k..n-1
+    double best = -1.0;
+    int bi = k;
+    for (int i = k + tid; i < n; i += NT) {
+      const double a = fabs(A[(long long)k * n + i]);
+      if (a > best) {
+        best = a;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if ((tid & 31) == 0) {
+      rv[tid >> 5] = best;
+      ri[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b2 = -1.0;
+      int i2 = k;
+      for (int w = 0; w < NT / 32; ++w)
+        if (rv[w] > b2 || (rv[w] == b2 && ri[w] < i2)) {
+          b2 = rv[w];
+          i2 = ri[w];
+        }
+      piv_s = i2;
+      perm[k] = i2;
+    }
+    __syncthreads();
+    const int p = piv_s;
+    if (p != k)
+      for (int j = tid; j < n; j += NT) {
+        const double t = A[(long long)j * n + k];
+        A[(long long)j * n + k] = A[(long long)j * n + p];
+        A[(long long)j * n + p] = t;
+      }
+    __syncthreads();
+    const double d = A[(long long)k * n + k];
+    const double dinv = d != 0.0 ? 1.0 / d : 0.0;
+    for (int j = tid; j < n; j += NT) {
+      rowk[j] = A[(long long)j * n + k];
+      colk[j] = A[(long long)k * n + j];
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int j = warp; j < n; j += NT / 32) {
+      double* Aj = A + (long long)j * n;
+      const double rj = rowk[j] * dinv;
+      for (int i = lane; i < n; i += 32) {
+        double v;
+        if (i == k) v = j == k ? dinv : rj;
+        else if (j == k) v = -colk[i] * dinv;
+        else v = Aj[i] - colk[i] * rj;
+        Aj[i] = v;
+      }
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, in reverse order
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p != k)
+      for (int i = tid; i < n; i += NT) {
+        const double t = A[(long long)k * n + i];
+        A[(long long)k * n + i] = A[(long long)p * n + i];
+        A[(long long)p * n + i] = t;
+      }
+    __syncthreads();
+  }
+}
+
 // row-major copy of the column-major inverses with the rows and columns of fixed DOFs zeroed
 __global__ void k_inv_rowmajor(const SysDesc* __restrict__ sys, const double* __restrict__ mask,
                                const long long* __restrict__ aoff, const double* __restrict__ Acm,
