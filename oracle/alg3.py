@@ -61,7 +61,10 @@ class DirichletLU:
 
 
 class Alg3:
-    def __init__(self, cfg: dict):
+    def __init__(self, cfg: dict, positions=None, regions=("p", "c")):
+        """positions: optional list of subdomain positions (lexicographic grid index) to set up and solve
+        (sampled parity at full size); regions: which regions' subdomains to set up.  Construction only: the
+        arithmetic of every solved subdomain is unchanged."""
         self.cfg = cfg
         self.d = d = cfg["dim"]
         self.prob = Problem(cfg)
@@ -74,6 +77,15 @@ class Alg3:
         self.grid_m = tuple(cfg["grid"])
         self.sub_p = M.subdomains(self.Gp, self.grid_m, ov)
         self.sub_c = M.subdomains(self.Gc, self.grid_m, ov)
+        if positions is not None:
+            keep = set(int(q) for q in positions)
+            lexpos = lambda sub: int(M.lex_index(np.asarray(sub.index), np.zeros(d, np.int64), np.asarray(self.grid_m)))
+            self.sub_p = [sb for sb in self.sub_p if lexpos(sb) in keep]
+            self.sub_c = [sb for sb in self.sub_c if lexpos(sb) in keep]
+        if "p" not in regions:
+            self.sub_p = []
+        if "c" not in regions:
+            self.sub_c = []
         # global fine node sets
         self.box_p = M.Box(self.Gp, (0,) * d, self.Gp.n)
         self.box_c = M.Box(self.Gc, (0,) * d, self.Gc.n)
