@@ -162,6 +162,7 @@ struct lpfem_ctx {
   long long coarse_n = 0;      // latest coarse time index available
   double coarse_dt = -1.0;
   bool overlap = true;
+  int coarse_newton = 1;  // coarse NS by Newton (same discrete solution as Picard, C11 tolerance); 0 = Picard
   cusolverDnHandle_t sol2 = nullptr;
   double *wpic = nullptr, *wpic2 = nullptr, *ppic = nullptr, *ppic2 = nullptr;
   double* nrm = nullptr;  // 2 doubles
@@ -589,6 +590,7 @@ __global__ void k_picard_norms(const double* u, const double* w, long long n, do
 template <class Kern, class... Args>
 void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Args&... a) {
   if (nsys == 0) return;
+  if (CL > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nsys * CL);
   cfg.blockDim = dim3(NT);
@@ -976,7 +978,8 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   const bool ml = lev == 1 && c->nl > 0;
   if (ml) coarse_box_inverses<D>(c, cu_new);
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
-  k_conduit_step<D><<<grid_rows(C.maxrows, ns), 128, 0, st>>>(C.ds, c->Lc[lev], cc, lev == 1 ? 1 : 0, c->kmult,
+  const int newton = lev == 1 ? 1 : c->coarse_newton;
+  k_conduit_step<D><<<grid_rows(C.maxrows, ns), 128, 0, st>>>(C.ds, c->Lc[lev], cc, newton, c->kmult,
                                                                c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), C.rowptr,
                                                                C.col, C.aconst, colscale, C.z, C.W, C.lag, C.qf, C.aux,
                                                                C.aout, C.rhs);
@@ -1030,9 +1033,12 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
     fetch_stats(c, c->fam[0][0], 0, true, dummy, ok);
   }
   const long long nu = (long long)D * c->n2c_c;
+  bool pic_ok = false;
+  const int newton0 = c->coarse_newton;
+  for (int attempt = 0; attempt < 2 && !pic_ok; ++attempt) {
+  if (attempt == 1) c->coarse_newton = 0;  // Newton failed: fall back to Picard from u^n
   CK(cudaMemcpyAsync(c->wpic, c->cu[so], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(c->ppic, c->cp[so], c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  bool pic_ok = false;
   for (int it = 0; it < c->opts.picard_max; ++it) {
     conduit_solve_once<D>(c, 0, t, c->wpic, c->ppic, c->cu[so], c->cst[so][2], c->wpic2, c->ppic2);
     double dummy = 0;
@@ -1046,12 +1052,15 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
     std::swap(c->ppic, c->ppic2);
     c->stats.picard_iters++;
     const double du = std::sqrt(hn[0]), un = std::sqrt(hn[1]);
+    if (!(du == du)) break;  // NaN: diverged
     if (du <= c->opts.picard_rtol * un || du <= 1e-14 * std::sqrt((double)nu)) {
       pic_ok = true;
       break;
     }
   }
-  if (!pic_ok) throw Err(LPFEM_ENOCONV, "coarse Picard iteration did not converge (C11)");
+  }
+  c->coarse_newton = newton0;
+  if (!pic_ok) throw Err(LPFEM_ENOCONV, "coarse Navier-Stokes iteration did not converge (C11)");
   if (!ok) {
     std::string m = "a coarse Krylov solve did not converge (C19) at n=" + std::to_string(n) + ":";
     for (int k = 0; k < 2; ++k)
@@ -1411,6 +1420,8 @@ void setup(lpfem_ctx* c) {
         const int nsys = std::max<int>(1, (int)F.hk.size());
         int cl = 1;
         while (cl < 8 && nsys * cl * 2 <= nsm) cl *= 2;
+        const char* ov = getenv(k == 0 ? "LPFEM_CLUSTER_POROUS" : "LPFEM_CLUSTER_CONDUIT");
+        if (ov && lev == 1) cl = std::max(1, std::min(16, atoi(ov)));
         F.cluster = cl;
       }
   }
@@ -1455,6 +1466,7 @@ void setup(lpfem_ctx* c) {
     if (cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
     cusolverDnSetStream(c->sol, st);
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evc[i], cudaEventDefault));
     if (cusolverDnCreate(&c->sol2) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
     cusolverDnSetStream(c->sol2, c->st2);
