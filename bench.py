@@ -229,8 +229,15 @@ def main():
         kr.append((t, b, n, name))
     t, b, n, name = max(kr)
     achieved = (b / max(n, 1)) / ((t / max(n, 1)) * 1e-3) / 1e9 if t > 0 else 0.0
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[f"{name}@{cfg['name']}"]
+        traffic = tr["dram_bytes_per_launch"]
+        traffic_src = tr["source"]
+    except Exception:
+        traffic_src = None
     roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+            "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
             "share_of_step": t / ms if ms > 0 else None,
             "algorithmic_bytes_per_launch": b / max(n, 1), "ms_per_launch": t / max(n, 1)}
     out = {

@@ -162,7 +162,10 @@ struct lpfem_ctx {
   long long coarse_n = 0;      // latest coarse time index available
   double coarse_dt = -1.0;
   bool overlap = true;
-  int coarse_newton = 1;  // coarse NS by Newton (same discrete solution as Picard, C11 tolerance); 0 = Picard
+  int coarse_newton = 1;
+  long long ml_built = -1;  // step at which the coarse-box inverses were last built
+  int ml_refresh = 1;       // rebuild period (steps)
+  double ml_dt = -1.0;  // coarse NS by Newton (same discrete solution as Picard, C11 tolerance); 0 = Picard
   cusolverDnHandle_t sol2 = nullptr;
   double *wpic = nullptr, *wpic2 = nullptr, *ppic = nullptr, *ppic2 = nullptr;
   double* nrm = nullptr;  // 2 doubles
@@ -976,7 +979,12 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   for (int a = 0; a < D; ++a) hmin = std::min(hmin, c->Lc[lev].G.hc[a]);
   const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
   const bool ml = lev == 1 && c->nl > 0;
-  if (ml) coarse_box_inverses<D>(c, cu_new);
+  // the coarse-box inverses only precondition the GMRES: 3D reuses them for ml_refresh steps
+  if (ml && (c->nstep - c->ml_built >= c->ml_refresh || c->ml_built < 0 || c->ml_dt != c->cur_dt)) {
+    coarse_box_inverses<D>(c, cu_new);
+    c->ml_built = c->nstep;
+    c->ml_dt = c->cur_dt;
+  }
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
   k_conduit_step<D><<<grid_rows(C.maxrows, ns), 128, 0, st>>>(C.ds, c->Lc[lev], cc, newton, c->kmult,
@@ -1467,6 +1475,8 @@ void setup(lpfem_ctx* c) {
     cusolverDnSetStream(c->sol, st);
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
+    c->ml_refresh = D == 2 ? 1 : 4;
+    if (getenv("LPFEM_ML_REFRESH")) c->ml_refresh = std::max(1, atoi(getenv("LPFEM_ML_REFRESH")));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evc[i], cudaEventDefault));
     if (cusolverDnCreate(&c->sol2) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
     cusolverDnSetStream(c->sol2, c->st2);
