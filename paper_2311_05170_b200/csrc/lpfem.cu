@@ -1261,6 +1261,15 @@ void setup(lpfem_ctx* c) {
     std::vector<int> rs;
     for (int r = 2; r < c->R; r *= 2)
       if (c->R % r == 0) rs.push_back(r);
+    if (const char* lv = getenv("LPFEM_ML_LEVELS")) {  // experiment: comma-separated intermediate ratios
+      rs.clear();
+      for (const char* q = lv; *q;) {
+        const int r = atoi(q);
+        if (r > 1 && r < c->R && c->R % r == 0 && (rs.empty() || r % rs.back() == 0)) rs.push_back(r);
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    }
     rs.push_back(c->R);
     if (aligned && (int)rs.size() <= NLMAX) {
       c->nl = (int)rs.size();
