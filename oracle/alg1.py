@@ -34,9 +34,18 @@ def coarse_cell_mult(cfg: dict, cells: np.ndarray, ratio: int) -> np.ndarray:
     return np.asarray(cfg["k_mult"])[M.lex_index(cH, np.zeros(d, np.int64), np.asarray(nH))]
 
 
-def solve_dirichlet(A: sp.csr_matrix, b: np.ndarray, fixed: np.ndarray, vals: np.ndarray, border=None):
+# Fill-reducing column orderings for SuperLU (no arithmetic difference: partial pivoting LU either way).
+# SPD porous systems: minimum degree on A^T + A.  Saddle-point systems (zero pressure diagonal, so SuperLU
+# pivots off the diagonal): minimum degree on A^T A, ~100x faster than A^T + A on a 64^2 Taylor-Hood box.
+ORDER_SPD = "MMD_AT_PLUS_A"
+ORDER_SADDLE = "MMD_ATA"
+
+
+def solve_dirichlet(A: sp.csr_matrix, b: np.ndarray, fixed: np.ndarray, vals: np.ndarray, border=None,
+                    spd: bool = True):
     """Solve A x = b with x[fixed] = vals (rows of fixed dofs dropped, columns moved to the RHS).
     border: optional dense column/row m over the free dofs (bordered Lagrange multiplier, C6)."""
+    order = ORDER_SPD if spd else ORDER_SADDLE
     free = ~fixed
     x = np.zeros(A.shape[0])
     x[fixed] = vals
@@ -47,10 +56,10 @@ def solve_dirichlet(A: sp.csr_matrix, b: np.ndarray, fixed: np.ndarray, vals: np
         n = Aff.shape[0]
         Aff = sp.bmat([[Aff, sp.csr_matrix(m[:, None])], [sp.csr_matrix(m[None, :]), None]]).tocsc()
         rhs = np.concatenate([rhs, [0.0]])
-        sol = spla.splu(Aff.tocsc(), permc_spec="MMD_AT_PLUS_A").solve(rhs)
+        sol = spla.splu(Aff.tocsc(), permc_spec=order).solve(rhs)
         x[free] = sol[:n]
         return x
-    x[free] = spla.splu(Aff.tocsc(), permc_spec="MMD_AT_PLUS_A").solve(rhs)
+    x[free] = spla.splu(Aff.tocsc(), permc_spec=order).solve(rhs)
     return x
 
 
@@ -220,7 +229,7 @@ class Alg1:
         w = u_n.copy()
         for it in range(self.picard_max):
             A_u = con.A_lin + con.fem.convection(w, eta)
-            x = solve_dirichlet(saddle(A_u, con.Bdiv), b, fixed, gvals)
+            x = solve_dirichlet(saddle(A_u, con.Bdiv), b, fixed, gvals, spd=False)
             u = x[: d * n2].reshape(d, n2)
             du = np.linalg.norm(u - w)
             w = u

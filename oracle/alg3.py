@@ -25,7 +25,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from . import mesh as M
-from .alg1 import Alg1, PorousOps, make_conduit_ops, saddle
+from .alg1 import ORDER_SADDLE, ORDER_SPD, Alg1, PorousOps, make_conduit_ops, saddle
 from .fem import prolongation
 from .mms import Problem
 
@@ -35,7 +35,7 @@ FIELDS = ("pF", "pf", "pm")
 class DirichletLU:
     """LU of A restricted to the free dofs, reused for many right-hand sides (porous: time-invariant)."""
 
-    def __init__(self, A: sp.csr_matrix, fixed: np.ndarray, border: np.ndarray | None = None):
+    def __init__(self, A: sp.csr_matrix, fixed: np.ndarray, border: np.ndarray | None = None, spd: bool = True):
         self.fixed = fixed
         self.free = free = ~fixed
         Aff = A[free][:, free]
@@ -45,7 +45,7 @@ class DirichletLU:
         if self.border:
             m = border[free]
             Aff = sp.bmat([[Aff, sp.csr_matrix(m[:, None])], [sp.csr_matrix(m[None, :]), None]])
-        self.lu = spla.splu(Aff.tocsc(), permc_spec="MMD_AT_PLUS_A")
+        self.lu = spla.splu(Aff.tocsc(), permc_spec=ORDER_SPD if spd else ORDER_SADDLE)
         self.Aff = Aff.tocsr()
 
     def solve(self, b: np.ndarray, vals: np.ndarray):
@@ -251,7 +251,7 @@ class Alg3:
         vals_full[:, dirn] = g - U[:, dirn]  # C5
         vals = np.concatenate([vals_full[a][fixed[a * n2:(a + 1) * n2]] for a in range(d)]
                               + [np.zeros(int(fixed[d * n2:].sum()))])
-        lu = DirichletLU(K, fixed, C["border"])
+        lu = DirichletLU(K, fixed, C["border"], spd=False)
         x = lu.solve(b, vals)
         C["last_rel_residual"] = lu.last_rel_residual
         e = x[: d * n2].reshape(d, n2)
