@@ -34,11 +34,13 @@ def coarse_cell_mult(cfg: dict, cells: np.ndarray, ratio: int) -> np.ndarray:
     return np.asarray(cfg["k_mult"])[M.lex_index(cH, np.zeros(d, np.int64), np.asarray(nH))]
 
 
-# Fill-reducing column orderings for SuperLU (no arithmetic difference: partial pivoting LU either way).
-# SPD porous systems: minimum degree on A^T + A.  Saddle-point systems (zero pressure diagonal, so SuperLU
-# pivots off the diagonal): minimum degree on A^T A, ~100x faster than A^T + A on a 64^2 Taylor-Hood box.
+# Fill-reducing column orderings for SuperLU (no arithmetic difference: the LU solves the same system).
+# SPD porous systems: minimum degree on A^T + A with diagonal pivots (no pivoting is needed for SPD matrices;
+# 6x faster on a 3D 18^3 P2 box).  Saddle-point systems (zero pressure diagonal, so SuperLU pivots off the
+# diagonal): minimum degree on A^T A, ~100x faster than A^T + A on a 64^2 Taylor-Hood box.
 ORDER_SPD = "MMD_AT_PLUS_A"
 ORDER_SADDLE = "MMD_ATA"
+PIVOT = {ORDER_SPD: 0.0, ORDER_SADDLE: 1.0}
 
 
 def solve_dirichlet(A: sp.csr_matrix, b: np.ndarray, fixed: np.ndarray, vals: np.ndarray, border=None,
@@ -56,10 +58,10 @@ def solve_dirichlet(A: sp.csr_matrix, b: np.ndarray, fixed: np.ndarray, vals: np
         n = Aff.shape[0]
         Aff = sp.bmat([[Aff, sp.csr_matrix(m[:, None])], [sp.csr_matrix(m[None, :]), None]]).tocsc()
         rhs = np.concatenate([rhs, [0.0]])
-        sol = spla.splu(Aff.tocsc(), permc_spec=order).solve(rhs)
+        sol = spla.splu(Aff.tocsc(), permc_spec=order, diag_pivot_thresh=PIVOT[order]).solve(rhs)
         x[free] = sol[:n]
         return x
-    x[free] = spla.splu(Aff.tocsc(), permc_spec=order).solve(rhs)
+    x[free] = spla.splu(Aff.tocsc(), permc_spec=order, diag_pivot_thresh=PIVOT[order]).solve(rhs)
     return x
 
 

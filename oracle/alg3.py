@@ -25,7 +25,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from . import mesh as M
-from .alg1 import ORDER_SADDLE, ORDER_SPD, Alg1, PorousOps, make_conduit_ops, saddle
+from .alg1 import ORDER_SADDLE, ORDER_SPD, PIVOT, Alg1, PorousOps, make_conduit_ops, saddle
 from .fem import prolongation
 from .mms import Problem
 
@@ -45,7 +45,8 @@ class DirichletLU:
         if self.border:
             m = border[free]
             Aff = sp.bmat([[Aff, sp.csr_matrix(m[:, None])], [sp.csr_matrix(m[None, :]), None]])
-        self.lu = spla.splu(Aff.tocsc(), permc_spec=ORDER_SPD if spd else ORDER_SADDLE)
+        order = ORDER_SPD if spd and border is None else ORDER_SADDLE
+        self.lu = spla.splu(Aff.tocsc(), permc_spec=order, diag_pivot_thresh=PIVOT[order])
         self.Aff = Aff.tocsr()
 
     def solve(self, b: np.ndarray, vals: np.ndarray):

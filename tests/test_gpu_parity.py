@@ -95,5 +95,6 @@ def test_parity_3d_small_mms():
     run_pair(cfg)
 
 
-def test_parity_cfg1_two_steps():
-    run_pair(I.config(1), steps=2)
+def test_parity_cfg1_full_trajectory():
+    worst, st = run_pair(I.config(1))
+    print("cfg1 worst", worst)
