@@ -57,10 +57,12 @@ def sampled_one_step(cfg, n, positions, regions=("p", "c"), tol=1e-9):
     return errs, cur
 
 
-def test_cfg2_sampled_one_step_parity():
-    # corner, edge and interior boxes of the 8x8 grid; step 4 (all three porous pressures non-zero, C16)
-    errs, _ = sampled_one_step(I.config(2), 4, positions=[0, 3, 27, 63])
-    print("cfg2", max(errs.values()))
+@pytest.mark.parametrize("n", [4, 20])
+def test_cfg2_sampled_one_step_parity(n):
+    # corner, edge and interior boxes of the 8x8 grid; step 4 (all three porous pressures non-zero, C16) and
+    # the last step of the configuration (20)
+    errs, _ = sampled_one_step(I.config(2), n, positions=[0, 3, 27, 63])
+    print("cfg2", n, max(errs.values()))
 
 
 def test_cfg3_sampled_one_step_parity():
