@@ -75,6 +75,7 @@ struct KArgs {
   int maxit;
   KStat* stat;
   long long* phase;  // LPFEM_PHASE_TIMERS only
+  double reorth2;    // GMRES: reorthogonalise when ||w'||^2 < reorth2 ||w||^2 (Kahan-Parlett: 0.5)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       cluster_sum(S, 1, par);
       double hn2 = S.fin[0];
       PHASE(4);
-      if (hn2 < 0.5 * ww) {
+      if (hn2 < A.reorth2 * ww) {
         // second projection (CGS2): h2 = V^T w', w'' = w' - V h2
         __syncthreads();
         dots_chunked<NT, M + 2>(S, V, ld, Vn, j + 1, 0, r0, r1);

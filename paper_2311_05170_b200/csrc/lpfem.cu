@@ -780,6 +780,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
+  a.reorth2 = getenv("LPFEM_REORTH2") ? atof(getenv("LPFEM_REORTH2")) : 0.5;
 #ifdef LPFEM_PHASE_TIMERS
   static long long* ph = nullptr;
   const int nsys_ph = (int)C.hk.size();
