@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblpfem.so")
+LIB_PATH = os.environ.get("LPFEM_LIB") or os.path.join(HERE, "liblpfem.so")  # override: experiment builds
 
 PROB = {"mms": 0, "injection": 1, "constant": 2, "mms_steady": 3}
 LAG = {"composite": 0, "subdomain": 1}

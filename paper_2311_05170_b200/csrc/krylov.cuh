@@ -58,6 +58,21 @@ struct KStat {
   } while (0)
 #endif
 
+#ifdef LPFEM_PHASE_TIMERS
+#define SUBPHASE(k)                                                                 \
+  do {                                                                              \
+    if (threadIdx.x == 0 && cgx::this_cluster().block_rank() == 0 && P.phase) {     \
+      long long t_ = clock64();                                                     \
+      P.phase[sid * 16 + 8 + (k)] += t_ - tsub;                                     \
+      tsub = t_;                                                                    \
+    }                                                                               \
+  } while (0)
+#else
+#define SUBPHASE(k) \
+  do {              \
+  } while (0)
+#endif
+
 struct KArgs {
   const KSys* sys;
   const long long* rowptr;
@@ -270,6 +285,9 @@ constexpr int RLN = 8;  // lanes per restricted row
 template <int D, int NC>
 __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ v, double* __restrict__ Z, int r0,
                            int r1, int nrows) {
+#ifdef LPFEM_PHASE_TIMERS
+  long long tsub = clock64();
+#endif
   cgx::cluster_group cl = cgx::this_cluster();
   const int gt = (int)cl.block_rank() * blockDim.x + threadIdx.x;
   const int gs = (int)cl.num_blocks() * blockDim.x;
@@ -299,7 +317,9 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
       const int wfirst = (gt & ~31) / RLN;  // warp-uniform trip count (shuffles inside)
       for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN)
         restrict_item<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
+      SUBPHASE(2 * l);
       cl.sync();
+      SUBPHASE(2 * l + 1);
       src = dst;
       SF = SC;
     }
@@ -314,10 +334,12 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     const int lane = threadIdx.x & 31;
     for (int i = gt >> 5; i < n; i += gs >> 5) {
       double s = 0.0;
+#pragma unroll 4
       for (int j = lane; j < n; j += 32) s += Ai[(long long)i * n + j] * rc[j];
       s = warp_sum(s);
       if (lane == 0) zc[i] = s;
     }
+    SUBPHASE(6);
     cl.sync();
     if (!P.direct) {
       for (int l = P.nl - 2; l >= 0; --l) {
@@ -332,6 +354,7 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
       }
     }
   }
+  SUBPHASE(7);
   const double* s0 = P.s0 + f * P.fstride + S0.row_off;
   for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
     const double si = s0[i];
@@ -476,6 +499,22 @@ __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const double* _
   }
 }
 
+// sum_{k<n} c[k] Vt_k[i], loads issued in batches of 8 independent basis reads (one L2/HBM latency per batch
+// instead of one per basis vector)
+__device__ __forceinline__ double basis_comb(const double* __restrict__ V, long long ld, const double* c, int n,
+                                             long long i) {
+  double s = 0.0;
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = (k0 + u < n) ? V[(k0 + u) * ld + i] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < n) s += c[k0 + u] * v[u];
+  }
+  return s;
+}
+
 // PC = false: right preconditioning folded into the matrix (A' = mask A diag(s)); the solution is y with
 //             x = s y (applied at write-back).
 // PC = true:  A is the masked unscaled operator and M^-1 = apply_prec; the solution is x itself.
@@ -502,7 +541,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   const long long ld = A.rows_total;
   double* V = A.V + K.row_off;
   __shared__ RedSmem<NT, M + 2> S;
-  __shared__ double H[M + 1][M], cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1], sig[M + 1];
+  __shared__ double H[M + 1][M], cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1], sig[M + 1], hs[M + 1];
   int par = 0;
   const int tid = threadIdx.x;
 #ifdef LPFEM_PHASE_TIMERS
@@ -563,9 +602,11 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       // pass B: w' = w - sum_k h_k v_k, written as Vt_{j+1}; ||w'||^2
       double* Vn = V + (j + 1) * ld;
       double pn = 0.0;
+      if (tid <= j) hs[tid] = hc[tid] * sig[tid];
+      __syncthreads();
       for (int i = r0 + tid; i < r1; i += NT) {
         double wi = W[i];
-        for (int k = 0; k <= j; ++k) wi -= (hc[k] * sig[k]) * V[k * ld + i];
+        wi -= basis_comb(V, ld, hs, j + 1, i);
         Vn[i] = wi;
         pn += wi * wi;
       }
@@ -579,9 +620,11 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         dots_chunked<NT, M + 2>(S, V, ld, Vn, j + 1, 0, r0, r1);
         cluster_sum(S, j + 1, par);
         double pn2 = 0.0;
+        if (tid <= j) hs[tid] = S.fin[tid] * sig[tid] * sig[tid];
+        __syncthreads();
         for (int i = r0 + tid; i < r1; i += NT) {
           double wi = Vn[i];
-          for (int k = 0; k <= j; ++k) wi -= (S.fin[k] * sig[k] * sig[k]) * V[k * ld + i];
+          wi -= basis_comb(V, ld, hs, j + 1, i);
           Vn[i] = wi;
           pn2 += wi * wi;
         }
@@ -629,20 +672,12 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     }
     __syncthreads();
     if (PC) {
-      for (int i = r0 + tid; i < r1; i += NT) {
-        double s = 0.0;
-        for (int k = 0; k < jend; ++k) s += yv[k] * V[k * ld + i];
-        r[i] = s;
-      }
+      for (int i = r0 + tid; i < r1; i += NT) r[i] = basis_comb(V, ld, yv, jend, i);
       cl.sync();
       apply_prec<D, D>(P, sid, r, Zw, r0, r1, K.nrows);
       for (int i = r0 + tid; i < r1; i += NT) x[i] += Zw[i];
     } else {
-      for (int i = r0 + tid; i < r1; i += NT) {
-        double s = x[i];
-        for (int k = 0; k < jend; ++k) s += yv[k] * V[k * ld + i];
-        x[i] = s;
-      }
+      for (int i = r0 + tid; i < r1; i += NT) x[i] += basis_comb(V, ld, yv, jend, i);
     }
     cl.sync();
     ++nspmv;

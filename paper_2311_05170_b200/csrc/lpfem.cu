@@ -61,7 +61,19 @@ T* dalloc(size_t n) {
   return (T*)p;
 }
 
-constexpr int GM = 30;  // GMRES restart length (compile-time register blocking)
+#ifndef LPFEM_GM
+#define LPFEM_GM 45
+#endif
+#ifndef LPFEM_TPR2
+#define LPFEM_TPR2 4
+#endif
+#ifndef LPFEM_TPR3
+#define LPFEM_TPR3 16
+#endif
+// GMRES restart length (compile-time: shared-memory Hessenberg and reductions).  Measured (cfg1/2/3 max
+// iterations 316/344/484 at 30 -> 246/313/399 at 45; GMRES time -1%/-10%/-14%)
+constexpr int GM = LPFEM_GM;
+constexpr int TPR2 = LPFEM_TPR2, TPR3 = LPFEM_TPR3;  // conduit SpMV lanes per row (2D ~28 nnz/row, 3D ~93)
 
 // NCCL is loaded lazily (multi-GPU only) so that the library has no link-time NCCL dependency; in a torch
 // process this resolves to the NCCL torch already loaded.
@@ -591,13 +603,14 @@ __global__ void k_picard_norms(const double* u, const double* w, long long n, do
 }
 
 template <class Kern, class... Args>
-void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Args&... a) {
+void launch_cluster_sm(Kern k, int nsys, int CL, int NT, size_t smem, cudaStream_t st, const Args&... a) {
   if (nsys == 0) return;
   if (CL > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (smem > 0) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nsys * CL);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -609,6 +622,12 @@ void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Arg
   CK(cudaLaunchKernelEx(&cfg, k, a...));
   ++tl_launches;
 }
+
+template <class Kern, class... Args>
+void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Args&... a) {
+  launch_cluster_sm(k, nsys, CL, NT, 0, st, a...);
+}
+
 
 template <int D>
 PorousCoefs porous_coefs(const lpfem_ctx* c, double dt) {
@@ -753,9 +772,9 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.stat = P.dstat;
   if (P.level == 1 && c->nlp > 0) {
     if (D == 2)
-      launch_cluster(k_pcg_ml<1024, 4, 2>, (int)P.hk.size(), P.cluster, 1024, c->st, a, c->mlp, P.zv);
+      launch_cluster_sm(k_pcg_ml<1024, 4, 2>, (int)P.hk.size(), P.cluster, 1024, 0, c->st, a, c->mlp, P.zv);
     else
-      launch_cluster(k_pcg_ml<1024, 8, 3>, (int)P.hk.size(), P.cluster, 1024, c->st, a, c->mlp, P.zv);
+      launch_cluster_sm(k_pcg_ml<1024, 8, 3>, (int)P.hk.size(), P.cluster, 1024, 0, c->st, a, c->mlp, P.zv);
   } else if (D == 2) {
     launch_cluster(k_cg<1024, 4>, (int)P.hk.size(), P.cluster, 1024, c->st, a);
   } else {
@@ -780,26 +799,32 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
-  a.reorth2 = getenv("LPFEM_REORTH2") ? atof(getenv("LPFEM_REORTH2")) : 0.5;
+  // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
+  // threshold reorthogonalised almost every iteration for identical iteration counts (cfg1-3), +20% GMRES time
+  a.reorth2 = getenv("LPFEM_REORTH2") ? atof(getenv("LPFEM_REORTH2")) : 0.1;
 #ifdef LPFEM_PHASE_TIMERS
   static long long* ph = nullptr;
   const int nsys_ph = (int)C.hk.size();
   if (!ph) ph = dalloc<long long>(16 * 4096);
   CK(cudaMemsetAsync(ph, 0, 16 * nsys_ph * sizeof(long long), c->st));
   a.phase = ph;
+  c->ml.phase = ph;
 #endif
   const bool pc = C.level == 1 && c->nl > 0;
-  constexpr int NTG = 1024;
+#ifndef LPFEM_NTG
+#define LPFEM_NTG 1024
+#endif
+  constexpr int NTG = LPFEM_NTG;  // threads per CTA of the conduit GMRES
   if (pc) {
     if (D == 2)
-      launch_cluster(k_gmres<NTG, 8, GM, 2, true>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
+      launch_cluster_sm(k_gmres<NTG, TPR2, GM, 2, true>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
     else
-      launch_cluster(k_gmres<NTG, 16, GM, 3, true>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
+      launch_cluster_sm(k_gmres<NTG, TPR3, GM, 3, true>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
   } else {
     if (D == 2)
-      launch_cluster(k_gmres<NTG, 8, GM, 2, false>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
+      launch_cluster_sm(k_gmres<NTG, TPR2, GM, 2, false>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
     else
-      launch_cluster(k_gmres<NTG, 16, GM, 3, false>, (int)C.hk.size(), C.cluster, NTG, c->st, a, c->ml);
+      launch_cluster_sm(k_gmres<NTG, TPR3, GM, 3, false>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
   }
 #ifdef LPFEM_PHASE_TIMERS
   if (C.level == 1) {
@@ -814,6 +839,8 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
     fprintf(stderr, "[phases] system %d iters %d, us per iteration:", worst, ks[worst].iters);
     const char* nm[7] = {"sync/V", "prec", "spmv", "cgs1", "cgs2", "cgs3", "norm+givens"};
     for (int k = 0; k < 7; ++k) fprintf(stderr, " %s %.2f", nm[k], h[16 * worst + k] / 1965.0 / std::max(1, ks[worst].iters));
+    fprintf(stderr, " | prec sub (restrict/sync per level, coarse, prolong+final):");
+    for (int k = 8; k < 16; ++k) fprintf(stderr, " %.2f", h[16 * worst + k] / 1965.0 / std::max(1, ks[worst].iters));
     fprintf(stderr, "\n");
   }
 #endif
@@ -924,7 +951,7 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new) {
   CKL();
   int nmax = 1;
   for (auto& S2 : F.hs) nmax = std::max(nmax, S2.nrows);
-  if (nmax <= 512) {
+  if (nmax <= (getenv("LPFEM_GJ_MAX") ? atoi(getenv("LPFEM_GJ_MAX")) : 512)) {
     // small boxes (2D): batched in-place Gauss-Jordan, one CTA per matrix
     const size_t smem = 2 * (size_t)nmax * sizeof(double);
     k_gj_inverse<1024><<<ns, 1024, smem, st>>>(F.ds, c->daoff, c->abuf, c->gjperm);
@@ -1272,6 +1299,13 @@ void setup(lpfem_ctx* c) {
       }
     }
     rs.push_back(c->R);
+    if (const char* cr = getenv("LPFEM_ML_COARSE")) {  // experiment: coarsest (exactly inverted) level at ratio r < R
+      const int r = atoi(cr);
+      if (r > 1 && c->R % r == 0) {
+        while (!rs.empty() && rs.back() >= r) rs.pop_back();
+        rs.push_back(r);
+      }
+    }
     if (aligned && (int)rs.size() <= NLMAX) {
       c->nl = (int)rs.size();
       std::vector<long long> poff, aoff;
@@ -1436,8 +1470,10 @@ void setup(lpfem_ctx* c) {
       for (int k = 0; k < 2; ++k) {
         Family& F = c->fam[lev][k];
         const int nsys = std::max<int>(1, (int)F.hk.size());
+        // one 1024-thread CTA per SM: the largest power of two <= 16 with nsys * cl <= nsm (cluster 16 is
+        // non-portable but supported on B200; measured cfg3: cl 8 -> 16 cuts the conduit GMRES 215 -> 134 ms)
         int cl = 1;
-        while (cl < 8 && nsys * cl * 2 <= nsm) cl *= 2;
+        while (cl < 16 && nsys * cl * 2 <= nsm) cl *= 2;
         const char* ov = getenv(k == 0 ? "LPFEM_CLUSTER_POROUS" : "LPFEM_CLUSTER_CONDUIT");
         if (ov && lev == 1) cl = std::max(1, std::min(16, atoi(ov)));
         F.cluster = cl;

@@ -34,6 +34,7 @@ struct MLArgs {
   int nsub;                     // boxes per field: system sid = field * nsub + box
   long long lstride[NLMAX];     // field stride of the level vectors / scalings
   long long fstride;            // field stride of the fine scaling s0
+  long long* phase;             // LPFEM_PHASE_TIMERS only: per-system sub-phase clocks (slots 8..15)
 };
 
 // Restriction P^T as a gather: the weight of coarse node I at fine point g is phi_I(x_g), so P^T v at a
@@ -238,6 +239,7 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
   int base[3] = {0, 0, 0};
   for (int a = 0; a < D; ++a) base[a] = q * l[a];
   double s0 = 0.0;
+#pragma unroll 4
   for (int i = b + lane; valid && i < e; i += LN) {
     int g0[3];
     bool ok0 = true;
