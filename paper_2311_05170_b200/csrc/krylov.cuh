@@ -91,7 +91,42 @@ struct KArgs {
   KStat* stat;
   long long* phase;  // LPFEM_PHASE_TIMERS only
   double reorth2;    // GMRES: reorthogonalise when ||w'||^2 < reorth2 ||w||^2 (Kahan-Parlett: 0.5)
+  int smem_cols;     // 1: every CTA stages its rows' pattern (row offsets + column indices) in shared memory
 };
+
+// Sparsity pattern of the CTA's rows [r0, r1): staged once per solve in dynamic shared memory when it fits (the
+// pattern is fixed for the whole Krylov solve; the SpMV then issues the value load and the x gather together,
+// one L2/HBM latency per batch instead of three dependent ones: rowptr -> col -> x).
+struct CtaPattern {
+  const long long* rp;  // global (system-offset rowptr), used when !sm
+  const int* col;
+  const double* val;
+  const int* srp;       // shared: row offsets relative to q0, nr + 1 entries
+  const int* scol;      // shared: column indices of the CTA's nonzeros
+  const double* sval;   // val + q0
+  bool sm;
+};
+
+template <int NT>
+__device__ __forceinline__ CtaPattern stage_pattern(const KArgs& A, const long long* rp, const double* val, int r0,
+                                                    int r1) {
+  extern __shared__ __align__(16) int lp_ksm[];
+  CtaPattern P{rp, A.col, val, nullptr, nullptr, nullptr, A.smem_cols != 0};
+  if (P.sm) {
+    const long long q0 = rp[r0];
+    const int nr = r1 - r0;
+    int* srp = lp_ksm;
+    int* scol = lp_ksm + ((nr + 4) & ~3);
+    for (int i = threadIdx.x; i <= nr; i += NT) srp[i] = (int)(rp[r0 + i] - q0);
+    const long long nq = rp[r1] - q0;
+    for (long long i = threadIdx.x; i < nq; i += NT) scol[i] = A.col[q0 + i];
+    __syncthreads();
+    P.srp = srp;
+    P.scol = scol;
+    P.sval = val + q0;
+  }
+  return P;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -107,21 +142,30 @@ struct RedSmem {
 };
 
 // Sum over the cluster of per-warp partials already stored in S.red[warp][0..n); returns via S.fin.
+// Stage 1: value k is reduced by warp k mod (NT/32) with a butterfly over the per-warp partials (lane w reads
+// red[w][k]); stage 2: thread k < n reads the cluster's CTA sums through DSMEM, all loads issued before the
+// fixed-order sum.  Deterministic (fixed order everywhere), two short latency chains instead of 32 + CL serial
+// loads on one thread.
 template <int NT, int NV>
 __device__ __forceinline__ void cluster_sum(RedSmem<NT, NV>& S, int n, int& par) {
+  static_assert(NT / 32 <= 32, "one lane per warp partial");
   cgx::cluster_group cl = cgx::this_cluster();
   __syncthreads();
-  const int tid = threadIdx.x;
-  if (tid < n) {
-    double s = 0.0;
-    for (int w = 0; w < NT / 32; ++w) s += S.red[w][tid];
-    S.cred[par][tid] = s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int k = warp; k < n; k += NT / 32) {
+    double v = lane < NT / 32 ? S.red[lane][k] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) S.cred[par][k] = v;
   }
   cl.sync();
   if (tid < n) {
-    double s = 0.0;
     const int nb = (int)cl.num_blocks();
-    for (int k = 0; k < nb; ++k) s += cl.map_shared_rank(&S.cred[par][0], k)[tid];
+    double t[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t[k] = k < nb ? cl.map_shared_rank(&S.cred[par][0], k)[tid] : 0.0;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += t[k];
     S.fin[tid] = s;
   }
   __syncthreads();
@@ -170,6 +214,48 @@ __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, cons
   }
 }
 
+// same with the pattern staged in shared memory (row r of the system is srp[r - r0] .. srp[r - r0 + 1])
+template <int NT, int TPR>
+__device__ __forceinline__ void spmv_rows_sm(const int* __restrict__ srp, const int* __restrict__ scol,
+                                             const double* __restrict__ sval, const double* __restrict__ x,
+                                             double* __restrict__ y, int r0, int r1) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x % TPR;
+  const int grp = threadIdx.x / TPR;
+  constexpr int NG = NT / TPR;
+  for (int base = r0; base < r1; base += NG) {
+    const int r = base + grp;
+    double s = 0.0;
+    if (r < r1) {
+      const int qb = srp[r - r0], qe = srp[r - r0 + 1];
+      for (int q0 = qb + lane; q0 < qe; q0 += TPR * U) {
+        double vv[U], xx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = q0 + u * TPR;
+          const bool in = q < qe;
+          vv[u] = in ? __ldg(sval + q) : 0.0;
+          xx[u] = in ? x[scol[q]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) s += vv[u] * xx[u];
+      }
+    }
+#pragma unroll
+    for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
+    if (r < r1 && lane == 0) y[r] = s;
+  }
+}
+
+template <int NT, int TPR>
+__device__ __forceinline__ void spmv(const CtaPattern& P, const double* __restrict__ x, double* __restrict__ y, int r0,
+                                     int r1) {
+  if (P.sm)
+    spmv_rows_sm<NT, TPR>(P.srp, P.scol, P.sval, x, y, r0, r1);
+  else
+    spmv_rows<NT, TPR>(P.rp, P.col, P.val, x, y, r0, r1);
+}
+
 // ---------------------------------------------------------------------------------------------
 template <int NT, int TPR>
 __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
@@ -189,6 +275,7 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
   double* r = A.r + K.row_off;
   double* p = A.p + K.row_off;
   double* q = A.q + K.row_off;
+  const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1);
   __shared__ RedSmem<NT, 2> S;
   int par = 0;
   const int tid = threadIdx.x;
@@ -216,7 +303,7 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
     int checks = 0;
     while (true) {
       cl.sync();  // p complete across the cluster
-      spmv_rows<NT, TPR>(rp, col, val, p, q, r0, r1);
+      spmv<NT, TPR>(PT, p, q, r0, r1);
       __syncthreads();
       double ppq = 0.0;
       for (int i = r0 + tid; i < r1; i += NT) ppq += p[i] * q[i];
@@ -241,7 +328,7 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
         // verify with the true residual r = b - A x
         ++nspmv;
         cl.sync();
-        spmv_rows<NT, TPR>(rp, col, val, x, q, r0, r1);
+        spmv<NT, TPR>(PT, x, q, r0, r1);
         __syncthreads();
         double pt = 0.0, pzz = 0.0;
         for (int i = r0 + tid; i < r1; i += NT) {
@@ -275,6 +362,7 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
     A.stat[sid].vsum = 0;
     A.stat[sid].spmv = it + nspmv;
   }
+  cl.sync();  // no CTA may exit while a peer still reads its shared memory (DSMEM, cluster_sum)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -399,6 +487,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
   double* p = A.p + K.row_off;
   double* q = A.q + K.row_off;
   double* z = zbuf + K.row_off;
+  const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1);
   __shared__ RedSmem<NT, 2> S;
   int par = 0;
   const int tid = threadIdx.x;
@@ -431,7 +520,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
     fresh = false;
     for (int i = r0 + tid; i < r1; i += NT) p[i] = z[i] + beta * p[i];
     cl.sync();
-    spmv_rows<NT, TPR>(rp, col, val, p, q, r0, r1);
+    spmv<NT, TPR>(PT, p, q, r0, r1);
     __syncthreads();
     double ppq = 0.0;
     for (int i = r0 + tid; i < r1; i += NT) ppq += p[i] * q[i];
@@ -452,7 +541,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
     if (S.fin[0] <= tol2 || it >= A.maxit || pq == 0.0) {
       ++nspmv;
       cl.sync();
-      spmv_rows<NT, TPR>(rp, col, val, x, q, r0, r1);
+      spmv<NT, TPR>(PT, x, q, r0, r1);
       __syncthreads();
       double pt = 0.0;
       for (int i = r0 + tid; i < r1; i += NT) {
@@ -475,6 +564,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
     A.stat[sid].vsum = 0;
     A.stat[sid].spmv = it + nspmv;
   }
+  cl.sync();  // no CTA may exit while a peer still reads its shared memory (DSMEM, cluster_sum)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -540,6 +630,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   double* Zw = PC ? A.q + K.row_off : nullptr;
   const long long ld = A.rows_total;
   double* V = A.V + K.row_off;
+  const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1);
   __shared__ RedSmem<NT, M + 2> S;
   __shared__ double H[M + 1][M], cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1], sig[M + 1], hs[M + 1];
   int par = 0;
@@ -572,16 +663,18 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     }
     int jend = 0;
     for (int j = 0; j < M; ++j) {
-      cl.sync();  // Vt_j complete, sig visible (smem written by thread 0 before the barrier)
+      // Vt_0 (and the restart's sig/gv) must be complete across the cluster; for j > 0 the norm reduction that
+      // closed iteration j - 1 (a cluster barrier after Vt_j was written) already guarantees it
+      if (j == 0) cl.sync();
       PHASE(0);
       const double sj = sig[j];
       if (PC) {
         apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);
-        spmv_rows<NT, TPR>(rp, col, val, Zw, W, r0, r1);
+        spmv<NT, TPR>(PT, Zw, W, r0, r1);
       } else {
-        spmv_rows<NT, TPR>(rp, col, val, V + j * ld, W, r0, r1);
+        spmv<NT, TPR>(PT, V + j * ld, W, r0, r1);
       }
       __syncthreads();
       PHASE(2);
@@ -638,14 +731,17 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       const double hn = sqrt(hn2);
       if (tid == 0) {
         sig[j + 1] = hn > 0.0 ? 1.0 / hn : 0.0;
-        for (int k = 0; k <= j; ++k) H[k][j] = hc[k];
-        H[j + 1][j] = hn;
+        // apply the previous rotations to column j; the running entry stays in a register (the serial chain is
+        // one rotation per step; cs, sn, hc loads are independent of it)
+        double a = hc[0];
         for (int k = 0; k < j; ++k) {
-          const double a = H[k][j], c = H[k + 1][j];
+          const double c = hc[k + 1];
           H[k][j] = cs[k] * a + sn[k] * c;
-          H[k + 1][j] = -sn[k] * a + cs[k] * c;
+          a = -sn[k] * a + cs[k] * c;
         }
-        const double a = H[j][j], c = H[j + 1][j];
+        H[j][j] = a;
+        H[j + 1][j] = hn;
+        const double c = hn;
         const double den = hypot(a, c);
         cs[j] = den > 0.0 ? a / den : 1.0;
         sn[j] = den > 0.0 ? c / den : 0.0;
@@ -681,7 +777,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     }
     cl.sync();
     ++nspmv;
-    spmv_rows<NT, TPR>(rp, col, val, x, W, r0, r1);
+    spmv<NT, TPR>(PT, x, W, r0, r1);
     __syncthreads();
     double pr = 0.0;
     for (int i = r0 + tid; i < r1; i += NT) {
@@ -702,6 +798,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     A.stat[sid].vsum = vsum;
     A.stat[sid].spmv = it + nspmv;
   }
+  cl.sync();  // no CTA may exit while a peer still reads its shared memory (DSMEM, cluster_sum)
 }
 
 }  // namespace lp

@@ -139,7 +139,10 @@ struct Family {
   KStat* dstat = nullptr;
   std::vector<KStat> hstat;
   int cluster = 1;
+  bool cluster_checked = false;  // cluster size reduced until all clusters are co-resident (resident_cluster)
+  bool bandwidth_bound = false;  // large systems: keep the largest cluster even if the launch needs two waves
   std::vector<long long> sys_nnz;        // nnz per Krylov system
+  std::vector<long long> hrp;            // host copy of rowptr (CTA pattern sizes for the Krylov launches)
   std::vector<int> sub_region, sub_pos;  // per local subdomain (fine)
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
@@ -356,6 +359,7 @@ void build_pattern(lpfem_ctx* c, Family& F) {
     std::vector<long long> rp(F.rows + 1);
     CK(cudaMemcpy(rp.data(), F.rowptr, (F.rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
     for (auto& S : F.hs) F.sys_nnz.push_back(rp[S.row_off + S.nrows] - rp[S.row_off]);
+    F.hrp = std::move(rp);
   }
   F.col = dalloc<int>(F.nnz);
   k_pattern_fill<D><<<grid_rows(F.maxrows, nsys), 128, 0, st>>>(F.ds, F.kind, F.rowptr, F.col);
@@ -623,9 +627,62 @@ void launch_cluster_sm(Kern k, int nsys, int CL, int NT, size_t smem, cudaStream
   ++tl_launches;
 }
 
+// Clusters of a Krylov launch wait on one another only inside a cluster, but the kernel ends with its slowest
+// system: every system's cluster must be resident at once, or the late ones run in a second wave (measured
+// cfg1: 16 clusters of 8 x 1024-thread CTAs -> one wave does not fit the GPCs, 21 ms instead of 13 ms).
+// Returns the largest cluster size <= CLmax whose clusters all fit (any size, not only powers of two: the GPCs
+// of a B200 are not all the same size), by the occupancy API.
+template <class Kern>
+int resident_cluster(Kern k, int nsys, int CLmax, int NT, size_t smem) {
+  for (int CL = CLmax; CL > 1; --CL) {
+    if (CL > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (smem > 0) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nsys * CL);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, (void*)k, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (getenv("LPFEM_VERBOSE")) fprintf(stderr, "[lpfem] cluster %d: %d systems, %d resident clusters\n", CL, nsys, ncl);
+    if (ncl >= nsys) return CL;
+  }
+  return 1;
+}
+
 template <class Kern, class... Args>
 void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Args&... a) {
   launch_cluster_sm(k, nsys, CL, NT, 0, st, a...);
+}
+
+// Dynamic shared memory for the CTA patterns staged by the Krylov kernels (krylov.cuh stage_pattern): the
+// largest (row offsets + column indices) of any CTA's row block, or 0 when one does not fit next to the
+// kernel's static shared memory (the kernels then read the pattern from global memory).
+template <class Kern>
+size_t pattern_smem(Kern k, const Family& F, int CL) {
+  if (getenv("LPFEM_NO_SMEM_PATTERN") || F.hrp.empty()) return 0;
+  cudaFuncAttributes at;
+  CK(cudaFuncGetAttributes(&at, k));
+  const long long budget = 227LL * 1024 - (long long)at.sharedSizeBytes - 1024;
+  long long need = 0;
+  for (const KSys& K : F.hk) {
+    const int chunk = (K.nrows + CL - 1) / CL;
+    for (int cr = 0; cr < CL; ++cr) {
+      const int r0 = std::min(K.nrows, cr * chunk), r1 = std::min(K.nrows, r0 + chunk);
+      const long long nq = F.hrp[K.prow_off + r1] - F.hrp[K.prow_off + r0];
+      need = std::max(need, 4LL * (((r1 - r0) + 4) & ~3) + 4 * nq);
+    }
+  }
+  return need <= budget ? (size_t)need : 0;
 }
 
 
@@ -770,15 +827,34 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.rtol = c->opts.krylov_rtol;
   a.maxit = c->opts.max_iter;
   a.stat = P.dstat;
+  const int ns = (int)P.hk.size();
+  auto go_ml = [&](auto k) {
+    if (!P.cluster_checked && !P.bandwidth_bound) {
+      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster));
+      P.cluster_checked = true;
+    }
+    const size_t sm = pattern_smem(k, P, P.cluster);
+    a.smem_cols = sm > 0;
+    launch_cluster_sm(k, ns, P.cluster, 1024, sm, c->st, a, c->mlp, P.zv);
+  };
+  auto go = [&](auto k) {
+    if (!P.cluster_checked && !P.bandwidth_bound) {
+      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster));
+      P.cluster_checked = true;
+    }
+    const size_t sm = pattern_smem(k, P, P.cluster);
+    a.smem_cols = sm > 0;
+    launch_cluster_sm(k, ns, P.cluster, 1024, sm, c->st, a);
+  };
   if (P.level == 1 && c->nlp > 0) {
     if (D == 2)
-      launch_cluster_sm(k_pcg_ml<1024, 4, 2>, (int)P.hk.size(), P.cluster, 1024, 0, c->st, a, c->mlp, P.zv);
+      go_ml(k_pcg_ml<1024, 4, 2>);
     else
-      launch_cluster_sm(k_pcg_ml<1024, 8, 3>, (int)P.hk.size(), P.cluster, 1024, 0, c->st, a, c->mlp, P.zv);
+      go_ml(k_pcg_ml<1024, 8, 3>);
   } else if (D == 2) {
-    launch_cluster(k_cg<1024, 4>, (int)P.hk.size(), P.cluster, 1024, c->st, a);
+    go(k_cg<1024, 4>);
   } else {
-    launch_cluster(k_cg<1024, 8>, (int)P.hk.size(), P.cluster, 1024, c->st, a);
+    go(k_cg<1024, 8>);
   }
 }
 
@@ -815,16 +891,25 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
 #define LPFEM_NTG 1024
 #endif
   constexpr int NTG = LPFEM_NTG;  // threads per CTA of the conduit GMRES
+  auto go = [&](auto k) {
+    if (!C.cluster_checked && !C.bandwidth_bound) {
+      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, pattern_smem(k, C, C.cluster));
+      C.cluster_checked = true;
+    }
+    const size_t sm = pattern_smem(k, C, C.cluster);
+    a.smem_cols = sm > 0;
+    launch_cluster_sm(k, (int)C.hk.size(), C.cluster, NTG, sm, c->st, a, c->ml);
+  };
   if (pc) {
     if (D == 2)
-      launch_cluster_sm(k_gmres<NTG, TPR2, GM, 2, true>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
+      go(k_gmres<NTG, TPR2, GM, 2, true>);
     else
-      launch_cluster_sm(k_gmres<NTG, TPR3, GM, 3, true>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
+      go(k_gmres<NTG, TPR3, GM, 3, true>);
   } else {
     if (D == 2)
-      launch_cluster_sm(k_gmres<NTG, TPR2, GM, 2, false>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
+      go(k_gmres<NTG, TPR2, GM, 2, false>);
     else
-      launch_cluster_sm(k_gmres<NTG, TPR3, GM, 3, false>, (int)C.hk.size(), C.cluster, NTG, 0, c->st, a, c->ml);
+      go(k_gmres<NTG, TPR3, GM, 3, false>);
   }
 #ifdef LPFEM_PHASE_TIMERS
   if (C.level == 1) {
@@ -836,6 +921,13 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
     int worst = 0;
     for (int i = 0; i < nsys_ph; ++i)
       if (ks[i].iters > ks[worst].iters) worst = i;
+    fprintf(stderr, "[phases] per system (iters, rows, in-loop ms):");
+    for (int i = 0; i < nsys_ph; ++i) {
+      long long tot = 0;
+      for (int k = 0; k < 7; ++k) tot += h[16 * i + k];
+      fprintf(stderr, " %d:(%d,%d,%.2f)", i, ks[i].iters, C.hk[i].nrows, tot / 1965.0 / 1000.0);
+    }
+    fprintf(stderr, "\n");
     fprintf(stderr, "[phases] system %d iters %d, us per iteration:", worst, ks[worst].iters);
     const char* nm[7] = {"sync/V", "prec", "spmv", "cgs1", "cgs2", "cgs3", "norm+givens"};
     for (int k = 0; k < 7; ++k) fprintf(stderr, " %s %.2f", nm[k], h[16 * worst + k] / 1965.0 / std::max(1, ks[worst].iters));
@@ -1470,10 +1562,19 @@ void setup(lpfem_ctx* c) {
       for (int k = 0; k < 2; ++k) {
         Family& F = c->fam[lev][k];
         const int nsys = std::max<int>(1, (int)F.hk.size());
-        // one 1024-thread CTA per SM: the largest power of two <= 16 with nsys * cl <= nsm (cluster 16 is
-        // non-portable but supported on B200; measured cfg3: cl 8 -> 16 cuts the conduit GMRES 215 -> 134 ms)
-        int cl = 1;
-        while (cl < 16 && nsys * cl * 2 <= nsm) cl *= 2;
+        // one 1024-thread CTA per SM: start from nsm / nsys (<= 16, non-portable above 8); the first Krylov
+        // launch lowers it until every cluster is resident at once (resident_cluster)
+        int cl = std::max(1, std::min(16, nsm / nsys));
+        // bandwidth-bound families (largest system > 2M nonzeros: cfg3's 3D boxes) keep the largest power of two
+        // and accept a second wave: measured cfg3 (8 systems) cluster 16 in 2 waves 107 ms vs cluster 10 in one
+        // wave 145 ms; latency-bound families (cfg1) need one wave: cluster 6 14.6 ms vs 8 in 2 waves 20 ms
+        long long nzmax = 0;
+        for (long long z : F.sys_nnz) nzmax = std::max(nzmax, z);
+        F.bandwidth_bound = nzmax > 2000000;
+        if (F.bandwidth_bound) {
+          cl = 1;
+          while (cl < 16 && nsys * cl * 2 <= nsm) cl *= 2;
+        }
         const char* ov = getenv(k == 0 ? "LPFEM_CLUSTER_POROUS" : "LPFEM_CLUSTER_CONDUIT");
         if (ov && lev == 1) cl = std::max(1, std::min(16, atoi(ov)));
         F.cluster = cl;
