@@ -206,6 +206,10 @@ struct lpfem_ctx {
   Family lvl[NLMAX];
   MLArgs ml{};
   double *part = nullptr, *aci = nullptr, *abuf = nullptr, *lwk = nullptr;
+  double* ainv[2] = {nullptr, nullptr};  // row-major coarse-box inverses, double-buffered (coarse_box_inverses)
+  int ml_next = 0, ml_busy = 0;          // slot the next fine step uses / slot the enqueued fine step reads
+  double* lwk2 = nullptr;                // cuSOLVER workspace of sol2 (coarse stream)
+  int *lpiv2 = nullptr, *linfo2 = nullptr;
   long long *dpoff = nullptr, *daoff = nullptr;
   std::vector<long long> haoff;
   int *lpiv = nullptr, *linfo = nullptr;
@@ -1012,8 +1016,11 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
 }
 
 // Newton-linearised operator of every coarse box (level L of the multilevel preconditioner), inverted densely.
+// Runs on the coarse stream (st2, cuSOLVER handle sol2) as the last part of coarse_step(n): U^{n+1} is known
+// there, so the inverses for fine step n are built while fine step n - 1 still runs.  The row-major result goes
+// to ainv[slot], double-buffered against the slot the running fine step reads.
 template <int D>
-void coarse_box_inverses(lpfem_ctx* c, const double* cu_new) {
+void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
   Family& F = c->lvl[c->nl - 1];
   const Level& L = c->Llv[c->nl - 1];
   const int ns = (int)F.hs.size();
@@ -1043,12 +1050,13 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new) {
   CKL();
   int nmax = 1;
   for (auto& S2 : F.hs) nmax = std::max(nmax, S2.nrows);
+  const double* cm = c->aci;  // column-major inverses
   if (nmax <= (getenv("LPFEM_GJ_MAX") ? atoi(getenv("LPFEM_GJ_MAX")) : 512)) {
     // small boxes (2D): batched in-place Gauss-Jordan, one CTA per matrix
     const size_t smem = 2 * (size_t)nmax * sizeof(double);
     k_gj_inverse<1024><<<ns, 1024, smem, st>>>(F.ds, c->daoff, c->abuf, c->gjperm);
     CKL();
-    std::swap(c->abuf, c->aci);  // aci: column-major inverses; abuf receives the row-major copy below
+    cm = c->abuf;
   } else {
     // large boxes (3D): dense LU per matrix (cuSOLVER), inverse by solving with the identity
     k_set_identity<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, c->daoff, c->aci);
@@ -1057,15 +1065,14 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new) {
       const int n = F.hs[s2].nrows;
       double* As = c->abuf + c->haoff[s2];
       double* Bs = c->aci + c->haoff[s2];
-      if (cusolverDnDgetrf(c->sol, n, n, As, n, c->lwk, c->lpiv, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+      if (cusolverDnDgetrf(c->sol2, n, n, As, n, c->lwk2, c->lpiv2, c->linfo2) != CUSOLVER_STATUS_SUCCESS)
         throw Err(LPFEM_ECUDA, "cusolverDnDgetrf (coarse box)");
-      if (cusolverDnDgetrs(c->sol, CUBLAS_OP_N, n, n, As, n, c->lpiv, Bs, n, c->linfo) != CUSOLVER_STATUS_SUCCESS)
+      if (cusolverDnDgetrs(c->sol2, CUBLAS_OP_N, n, n, As, n, c->lpiv2, Bs, n, c->linfo2) != CUSOLVER_STATUS_SUCCESS)
         throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (coarse box)");
     }
   }
-  k_inv_rowmajor<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, c->aci, c->abuf);
+  k_inv_rowmajor<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, cm, c->ainv[slot]);
   CKL();
-  c->ml.aci = c->abuf;
 }
 
 template <int D>
@@ -1099,11 +1106,9 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   for (int a = 0; a < D; ++a) hmin = std::min(hmin, c->Lc[lev].G.hc[a]);
   const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
   const bool ml = lev == 1 && c->nl > 0;
-  // the coarse-box inverses only precondition the GMRES: 3D reuses them for ml_refresh steps
-  if (ml && (c->nstep - c->ml_built >= c->ml_refresh || c->ml_built < 0 || c->ml_dt != c->cur_dt)) {
-    coarse_box_inverses<D>(c, cu_new);
-    c->ml_built = c->nstep;
-    c->ml_dt = c->cur_dt;
+  if (ml) {  // coarse-box inverses built by coarse_step (coarse stream, one step ahead)
+    c->ml_busy = c->ml_next;
+    c->ml.aci = c->ainv[c->ml_busy];
   }
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
@@ -1199,6 +1204,16 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
   }
   CK(cudaMemcpyAsync(c->cu[sn], c->wpic, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(c->cp[sn], c->ppic, c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  // coarse-box inverses of the multilevel preconditioner for fine step n (Newton-linearised at U = P u_H^{n+1};
+  // 3D reuses them for ml_refresh steps), into the slot the in-flight fine step does not read
+  if (c->nl > 0 && !c->fam[1][1].hs.empty() &&
+      (n - c->ml_built >= c->ml_refresh || c->ml_built < 0 || c->ml_dt != dt)) {
+    const int slot = 1 - c->ml_busy;
+    coarse_box_inverses<D>(c, c->cu[sn], slot);
+    c->ml_next = slot;
+    c->ml_built = n;
+    c->ml_dt = dt;
+  }
   CK(cudaEventRecord(c->evc[1], st));
   CK(cudaEventSynchronize(c->evc[1]));
   float ms = 0;
@@ -1463,6 +1478,8 @@ void setup(lpfem_ctx* c) {
       c->part = dalloc<double>(ptot);
       c->aci = dalloc<double>(atot);
       c->abuf = dalloc<double>(atot);
+      c->ainv[0] = dalloc<double>(atot);
+      c->ainv[1] = dalloc<double>(atot);
       c->gjperm = dalloc<int>(atot);
       c->dpoff = dalloc<long long>(poff.size());
       c->daoff = dalloc<long long>(aoff.size());
@@ -1641,6 +1658,9 @@ void setup(lpfem_ctx* c) {
       if (cusolverDnDgetrf_bufferSize(c->sol, nmax, nmax, c->abuf, nmax, &c->llwork) != CUSOLVER_STATUS_SUCCESS)
         throw Err(LPFEM_ECUDA, "cusolverDnDgetrf_bufferSize");
       c->lwk = dalloc<double>(std::max(1, c->llwork));
+      c->lwk2 = dalloc<double>(std::max(1, c->llwork));
+      c->lpiv2 = dalloc<int>(nmax + 4096);
+      c->linfo2 = dalloc<int>(1);
     }
   }
   for (int i = 0; i < 4; ++i) {
@@ -2183,7 +2203,8 @@ void lpfem_destroy(lpfem_ctx* c) {
   if (c->gbuf) cudaFree(c->gbuf);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   {
-    void* mp[] = {c->gjperm, c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo};
+    void* mp[] = {c->gjperm, c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo,
+                  c->ainv[0], c->ainv[1], c->lwk2, c->lpiv2, c->linfo2};
     for (void* p : mp)
       if (p) cudaFree(p);
   }
