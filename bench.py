@@ -52,7 +52,7 @@ METRIC = "fine DOF*steps/s (Algorithm 3 step: coarse + local subdomain correctio
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region (200 ms period)."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed region (50 ms period)."""
 
     def __init__(self, index: int):
         self.index = index
@@ -65,7 +65,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()

@@ -73,6 +73,10 @@ T* dalloc(size_t n) {
 // GMRES restart length (compile-time: shared-memory Hessenberg and reductions).  Measured (cfg1/2/3 max
 // iterations 316/344/484 at 30 -> 246/313/399 at 45; GMRES time -1%/-10%/-14%)
 constexpr int GM = LPFEM_GM;
+#ifndef LPFEM_NTG
+#define LPFEM_NTG 1024
+#endif
+constexpr int NTG = LPFEM_NTG;  // threads per CTA of the conduit GMRES
 constexpr int TPR2 = LPFEM_TPR2, TPR3 = LPFEM_TPR3;  // conduit SpMV lanes per row (2D ~28 nnz/row, 3D ~93)
 
 // NCCL is loaded lazily (multi-GPU only) so that the library has no link-time NCCL dependency; in a torch
@@ -173,6 +177,9 @@ struct lpfem_ctx {
   double* cu[3] = {};
   double* cp[3] = {};
   cudaStream_t st2 = nullptr;  // coarse marching stream (overlaps the fine stage)
+  int nsm = 148;               // SMs of the device
+  cudaStream_t st3 = nullptr;  // fine porous stage, concurrent with the fine conduit stage (independent)
+  cudaEvent_t evp[2] = {};     // fork / join of st3
   cudaEvent_t evc[3] = {};
   long long coarse_n = 0;      // latest coarse time index available
   double coarse_dt = -1.0;
@@ -891,10 +898,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   c->ml.phase = ph;
 #endif
   const bool pc = C.level == 1 && c->nl > 0;
-#ifndef LPFEM_NTG
-#define LPFEM_NTG 1024
-#endif
-  constexpr int NTG = LPFEM_NTG;  // threads per CTA of the conduit GMRES
+
   auto go = [&](auto k) {
     if (!C.cluster_checked && !C.bandwidth_bound) {
       C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, pattern_smem(k, C, C.cluster));
@@ -940,6 +944,33 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
     fprintf(stderr, "\n");
   }
 #endif
+}
+
+// Cluster sizes of the fine Krylov launches, decided before the first fine stage: the conduit GMRES first (all its
+// clusters resident), then the porous PCG, which runs concurrently on st3, gets the SMs the conduit leaves free.
+template <int D>
+void decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
+  Family& C = c->fam[1][1];
+  Family& P = c->fam[1][0];
+  if (!C.hk.empty() && !C.cluster_checked && !C.bandwidth_bound) {
+    auto chk = [&](auto k) {
+      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, pattern_smem(k, C, C.cluster));
+      C.cluster_checked = true;
+    };
+    const bool pc = c->nl > 0;
+    if (D == 2) {
+      if (pc) chk(k_gmres<NTG, TPR2, GM, 2, true>);
+      else chk(k_gmres<NTG, TPR2, GM, 2, false>);
+    } else {
+      if (pc) chk(k_gmres<NTG, TPR3, GM, 3, true>);
+      else chk(k_gmres<NTG, TPR3, GM, 3, false>);
+    }
+  }
+  if (concurrent && !P.hk.empty() && !P.cluster_checked && !P.bandwidth_bound && !C.hk.empty() &&
+      !C.bandwidth_bound) {
+    const int left = c->nsm - (int)C.hk.size() * C.cluster;
+    P.cluster = std::max(1, std::min(P.cluster, left / (int)P.hk.size()));
+  }
 }
 
 void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres, bool& ok) {
@@ -1247,8 +1278,22 @@ void do_step(lpfem_ctx* c, double dt) {
   const int so = (int)(n % 3), sn = (int)((n + 1) % 3);
   // ---------------- Steps 3-4: fine corrections + write-back
   CK(cudaEventRecord(c->ev[1], st));
-  porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+  // the porous and conduit corrections of a step are independent (each reads only coarse data and its own
+  // region's lagged composite): LPFEM_CONCURRENT=1 runs the porous stage on st3 beside the conduit stage.  Off by
+  // default: measured cfg1 17.5 vs 17.4 ms, cfg2 206 vs 213 ms, cfg3 equal (the GMRES slows by what the PCG saves)
+  const bool conc = c->st3 && getenv("LPFEM_CONCURRENT");
+  decide_fine_clusters<D>(c, conc);
+  if (conc) {
+    CK(cudaEventRecord(c->evp[0], st));
+    CK(cudaStreamWaitEvent(c->st3, c->evp[0], 0));
+    StreamSwap sw(c, c->st3);
+    porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+    CK(cudaEventRecord(c->evp[1], c->st3));
+  } else {
+    porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+  }
   conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp_u, c->comp_p);
+  if (conc) CK(cudaStreamWaitEvent(st, c->evp[1], 0));
   halo_exchange(c);  // a11: refresh the overlaps of the lagged fields (C2 mode B), world > 1 only
   CK(cudaEventRecord(c->ev[2], st));
   // ---------------- Step 1 of the next step, overlapped with this fine stage (reads slot n+1, writes n+2)
@@ -1575,6 +1620,7 @@ void setup(lpfem_ctx* c) {
     int nsm = 148;
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, c->dist.device) == cudaSuccess) nsm = prop.multiProcessorCount;
+    c->nsm = nsm;
     for (int lev = 0; lev < 2; ++lev)
       for (int k = 0; k < 2; ++k) {
         Family& F = c->fam[lev][k];
@@ -1638,6 +1684,8 @@ void setup(lpfem_ctx* c) {
     if (cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
     cusolverDnSetStream(c->sol, st);
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
     if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
     c->ml_refresh = D == 2 ? 1 : 4;
     if (getenv("LPFEM_ML_REFRESH")) c->ml_refresh = std::max(1, atoi(getenv("LPFEM_ML_REFRESH")));
@@ -2202,6 +2250,8 @@ void lpfem_destroy(lpfem_ctx* c) {
   }
   if (c->gbuf) cudaFree(c->gbuf);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  if (c->st2) cudaStreamSynchronize(c->st2);
+  if (c->st3) cudaStreamSynchronize(c->st3);
   {
     void* mp[] = {c->gjperm, c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo,
                   c->ainv[0], c->ainv[1], c->lwk2, c->lpiv2, c->linfo2};
@@ -2214,6 +2264,9 @@ void lpfem_destroy(lpfem_ctx* c) {
     cudaStreamSynchronize(c->st2);
     cudaStreamDestroy(c->st2);
   }
+  if (c->st3) cudaStreamDestroy(c->st3);
+  for (int i = 0; i < 2; ++i)
+    if (c->evp[i]) cudaEventDestroy(c->evp[i]);
   for (int i = 0; i < 3; ++i)
     if (c->evc[i]) cudaEventDestroy(c->evc[i]);
   void* ptrs[] = {c->dense, c->dwork, c->piv, c->dinfo, c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
