@@ -108,6 +108,8 @@ typedef struct {
   double t_krylov_ms[2];           /* cumulative device time of the fine Krylov launches [PCG, GMRES] (CUDA events) */
   double bytes_krylov[2];          /* cumulative algorithmic bytes of those launches ("Roofline") */
   long long krylov_launches[2];    /* number of fine Krylov launches */
+  long long coarse_factorizations; /* cumulative dense LU factorisations of the coarse Navier-Stokes Jacobian
+                                      (chord iteration reuses the last one while it contracts) */
 } lpfem_stats;
 
 /* NCCL unique id for a multi-GPU ctx (rank 0 only; world > 1). */

@@ -64,7 +64,7 @@ class Stats(C.Structure):
                 ("n_systems", C.c_longlong * 2), ("n_rows", C.c_longlong * 2), ("nnz", C.c_longlong * 2),
                 ("fine_dofs", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("t_krylov_ms", C.c_double * 2), ("bytes_krylov", C.c_double * 2),
-                ("krylov_launches", C.c_longlong * 2)]
+                ("krylov_launches", C.c_longlong * 2), ("coarse_factorizations", C.c_longlong)]
 
 
 class LPFEMError(RuntimeError):

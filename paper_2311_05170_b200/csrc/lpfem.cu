@@ -138,6 +138,7 @@ struct Family {
   // vectors
   double *base = nullptr, *z = nullptr, *lag = nullptr, *qf = nullptr, *aux = nullptr, *W = nullptr;
   double *rhs = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *V = nullptr, *ecorr = nullptr;
+  double *h1 = nullptr, *h2 = nullptr;  // hybrid preconditioner work vectors (conduit, fine)
   std::vector<KSys> hk;
   KSys* dk = nullptr;
   KStat* dstat = nullptr;
@@ -151,7 +152,7 @@ struct Family {
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
     void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, dinv, zv, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
-                    rhs, x, r, p, q, V, ecorr, dk, dstat};
+                    rhs, x, r, p, q, V, ecorr, dk, dstat, h1, h2};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
   }
@@ -215,6 +216,10 @@ struct lpfem_ctx {
   double *part = nullptr, *aci = nullptr, *abuf = nullptr, *lwk = nullptr;
   double* ainv[2] = {nullptr, nullptr};  // row-major coarse-box inverses, double-buffered (coarse_box_inverses)
   int ml_next = 0, ml_busy = 0;          // slot the next fine step uses / slot the enqueued fine step reads
+  // coarse Navier-Stokes chord iteration: LU of the last factorised Jacobian in `dense`/`piv` (conduit_solve_once)
+  bool clu_valid = false, clu_force = false;
+  int clu_newton = -1;
+  double clu_dt = -1.0;
   double* lwk2 = nullptr;                // cuSOLVER workspace of sol2 (coarse stream)
   int *lpiv2 = nullptr, *linfo2 = nullptr;
   long long *dpoff = nullptr, *daoff = nullptr;
@@ -402,6 +407,10 @@ void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
     F.mask = dalloc<double>(F.rows);
     F.W = dalloc<double>(F.rows);
     F.q = dalloc<double>(F.rows);
+    if (!level_family && F.level == 1) {
+      F.h1 = dalloc<double>(F.rows);
+      F.h2 = dalloc<double>(F.rows);
+    }
     if (!level_family) F.V = dalloc<double>((size_t)(GM + 1) * F.rows);
   }
   if (level_family) return;
@@ -886,6 +895,9 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
+  a.hybrid = (C.level == 1 && c->nl > 0 && getenv("LPFEM_ML_HYBRID")) ? atoi(getenv("LPFEM_ML_HYBRID")) : 0;
+  a.h1 = C.h1;
+  a.h2 = C.h2;
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
   // threshold reorthogonalised almost every iteration for identical iteration counts (cfg1-3), +20% GMRES time
   a.reorth2 = getenv("LPFEM_REORTH2") ? atof(getenv("LPFEM_REORTH2")) : 0.1;
@@ -1149,13 +1161,25 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
                                                                C.aout, C.rhs);
   CKL();
   if (lev == 0) {
+    // The system is in correction form around the current iterate z (rhs = b(W) - J(W) z, the nonlinear
+    // residual), so any nonsingular matrix gives a convergent fixed-point map near the solution when it is
+    // close to J: the chord iteration keeps the LU of the last factorised Jacobian while the iteration
+    // contracts (coarse_step decides), and converges to the same discrete solution under the same C11 test.
     const int n = (int)C.rows;
-    CK(cudaMemsetAsync(c->dense, 0, (size_t)n * n * sizeof(double), st));
-    k_csr_to_dense<<<(n + 127) / 128, 128, 0, st>>>(C.rowptr, C.col, C.aout, C.scale, n, c->dense);
-    CKL();
+    const bool reuse = c->clu_valid && !c->clu_force && c->clu_newton == newton && c->clu_dt == c->cur_dt;
+    if (!reuse) {
+      CK(cudaMemsetAsync(c->dense, 0, (size_t)n * n * sizeof(double), st));
+      k_csr_to_dense<<<(n + 127) / 128, 128, 0, st>>>(C.rowptr, C.col, C.aout, C.scale, n, c->dense);
+      CKL();
+      if (cusolverDnDgetrf(c->sol2, n, n, c->dense, n, c->dwork, c->piv, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
+        throw Err(LPFEM_ECUDA, "cusolverDnDgetrf");
+      c->clu_valid = true;
+      c->clu_force = false;
+      c->clu_newton = newton;
+      c->clu_dt = c->cur_dt;
+      c->stats.coarse_factorizations++;
+    }
     CK(cudaMemcpyAsync(C.x, C.rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (cusolverDnDgetrf(c->sol2, n, n, c->dense, n, c->dwork, c->piv, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
-      throw Err(LPFEM_ECUDA, "cusolverDnDgetrf");
     if (cusolverDnDgetrs(c->sol2, CUBLAS_OP_N, n, 1, c->dense, n, c->piv, C.x, n, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
       throw Err(LPFEM_ECUDA, "cusolverDnDgetrs");
     KStat ks{};
@@ -1203,6 +1227,8 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
   if (attempt == 1) c->coarse_newton = 0;  // Newton failed: fall back to Picard from u^n
   CK(cudaMemcpyAsync(c->wpic, c->cu[so], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(c->ppic, c->cp[so], c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  double du_prev = 0.0;
+  if (attempt == 1) c->clu_force = true;
   for (int it = 0; it < c->opts.picard_max; ++it) {
     conduit_solve_once<D>(c, 0, t, c->wpic, c->ppic, c->cu[so], c->cst[so][2], c->wpic2, c->ppic2);
     double dummy = 0;
@@ -1217,6 +1243,10 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
     c->stats.picard_iters++;
     const double du = std::sqrt(hn[0]), un = std::sqrt(hn[1]);
     if (!(du == du)) break;  // NaN: diverged
+    // chord iteration: refactorise at the current iterate when the frozen Jacobian contracts too slowly
+    // (or diverges); LPFEM_COARSE_FULL_NEWTON refactorises every iteration (plain Newton / Picard)
+    if (getenv("LPFEM_COARSE_FULL_NEWTON") || (it > 0 && du > 0.25 * du_prev) || it >= 12) c->clu_force = true;
+    du_prev = du;
     if (du <= c->opts.picard_rtol * un || du <= 1e-14 * std::sqrt((double)nu)) {
       pic_ok = true;
       break;
