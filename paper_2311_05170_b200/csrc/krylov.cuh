@@ -92,10 +92,6 @@ struct KArgs {
   long long* phase;  // LPFEM_PHASE_TIMERS only
   double reorth2;    // GMRES: reorthogonalise when ||w'||^2 < reorth2 ||w||^2 (Kahan-Parlett: 0.5)
   int smem_cols;     // 1: every CTA stages its rows' pattern (row offsets + column indices) in shared memory
-  int hybrid;        // GMRES preconditioner: 0 additive multilevel; 1 multiplicative coarse correction + additive
-                     // levels on the residual; 2 multiplicative coarse correction + fine scaling only
-  double* h1;        // hybrid: system-local work vectors (coarse correction z1, residual t)
-  double* h2;
 };
 
 // Sparsity pattern of the CTA's rows [r0, r1): staged once per solve in dynamic shared memory when it fits (the
@@ -468,100 +464,6 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
   (void)nrows;
 }
 
-// Hybrid multilevel preconditioner (experiment, KArgs.hybrid): the exact coarse-box correction applied
-// multiplicatively, the additive part on the remaining residual:
-//     z1 = C v,  C = P_L A_L^-1 R_L (restriction down the level chain, coarse solve, prolongation up, no scalings)
-//     t  = v - A z1
-//     z  = z1 + S_0 t + sum_{l<L} P_l S_l R_l t      (hybrid = 1)   or   z = z1 + S_0 t   (hybrid = 2)
-// Fixed rows (S_0 = 0) get z = 0, as in apply_prec.
-template <int NT, int TPR, int D, int NC>
-__device__ void apply_prec_hybrid(const MLArgs& P, int sid, const double* __restrict__ v, double* __restrict__ Z,
-                                  int r0, int r1, const CtaPattern& PT, double* __restrict__ z1,
-                                  double* __restrict__ t, int mode) {
-  cgx::cluster_group cl = cgx::this_cluster();
-  const int gt = (int)cl.block_rank() * blockDim.x + threadIdx.x;
-  const int gs = (int)cl.num_blocks() * blockDim.x;
-  const int f = sid / P.nsub, bx = sid % P.nsub;
-  const SysDesc S0 = P.fsys[bx];
-  const int L = P.nl - 1;
-  auto LRp = [&](int l) { return P.LR[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
-  auto LZp = [&](int l) { return P.LZ[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
-  auto LSp = [&](int l) { return P.LS[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
-  const double* s0 = P.s0 + f * P.fstride + S0.row_off;
-  auto restrict_down = [&](const double* src, int lmax) {
-    SysDesc SF = S0;
-    for (int l = 0; l <= lmax; ++l) {
-      const SysDesc SC = P.lsys[l][bx];
-      double* dst = LRp(l);
-      const int wfirst = (gt & ~31) / RLN;
-      for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN)
-        restrict_item<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
-      cl.sync();
-      src = dst;
-      SF = SC;
-    }
-  };
-  // ---- z1 = C v
-  restrict_down(v, L);
-  {
-    const int n = P.lsys[L][bx].nrows;
-    const double* Ai = P.aci + P.aoff[sid];
-    const double* rc = LRp(L);
-    double* zc = LZp(L);
-    const int lane = threadIdx.x & 31;
-    for (int i = gt >> 5; i < n; i += gs >> 5) {
-      double a = 0.0;
-#pragma unroll 4
-      for (int j = lane; j < n; j += 32) a += Ai[(long long)i * n + j] * rc[j];
-      a = warp_sum(a);
-      if (lane == 0) zc[i] = a;
-    }
-    cl.sync();
-  }
-  for (int l = L - 1; l >= 0; --l) {
-    const SysDesc SL = P.lsys[l][bx], SU = P.lsys[l + 1][bx];
-    double* zl = LZp(l);
-    const double* zu = LZp(l + 1);
-    for (int i = gt; i < SL.nrows; i += gs) zl[i] = prolong_row<D, NC>(SL, SU, P.q[l + 1], zu, i);
-    cl.sync();
-  }
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x)
-    z1[i] = s0[i] != 0.0 ? prolong_row<D, NC>(S0, P.lsys[0][bx], P.q[0], LZp(0), i) : 0.0;
-  cl.sync();
-  // ---- t = v - A z1
-  spmv<NT, TPR>(PT, z1, t, r0, r1);
-  __syncthreads();
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) t[i] = v[i] - t[i];
-  if (mode == 2 || L == 0) {
-    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) Z[i] = s0[i] != 0.0 ? z1[i] + s0[i] * t[i] : 0.0;
-    return;
-  }
-  cl.sync();
-  // ---- z = z1 + S_0 t + sum_{l<L} P_l S_l R_l t
-  restrict_down(t, L - 1);
-  {
-    const SysDesc SL = P.lsys[L - 1][bx];
-    const double* rl = LRp(L - 1);
-    const double* sl = LSp(L - 1);
-    double* zl = LZp(L - 1);
-    for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i];
-    cl.sync();
-  }
-  for (int l = L - 2; l >= 0; --l) {
-    const SysDesc SL = P.lsys[l][bx], SU = P.lsys[l + 1][bx];
-    const double* rl = LRp(l);
-    const double* sl = LSp(l);
-    double* zl = LZp(l);
-    const double* zu = LZp(l + 1);
-    for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i] + prolong_row<D, NC>(SL, SU, P.q[l + 1], zu, i);
-    cl.sync();
-  }
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    const double si = s0[i];
-    Z[i] = si != 0.0 ? z1[i] + si * t[i] + prolong_row<D, NC>(S0, P.lsys[0][bx], P.q[0], LZp(0), i) : 0.0;
-  }
-}
-
 // ---------------------------------------------------------------------------------------------
 // Preconditioned CG with the multilevel preconditioner (porous systems, SPD): unscaled masked operator,
 // z = M^-1 r (symmetric: restriction = transpose of the prolongation), stopping test on the unscaled residual
@@ -667,10 +569,15 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
 
 // ---------------------------------------------------------------------------------------------
 // Dot products h_k = sum_i Vt_k[i] w[i] (k < nk) of the rows [r0, r1) into the per-warp partials S.red[.][k0+k],
-// in chunks of 8 basis vectors (8 accumulators in registers; w is re-read once per chunk).
+// in chunks of 8 basis vectors (8 accumulators in registers; w is re-read once per chunk).  The 8 warp sums of
+// a chunk are formed by a reduce-scatter butterfly (xor 4, 2, 1: lane l keeps value l & 7) followed by two
+// shuffles across the lane octets: 9 shuffles per chunk instead of 8 x 5.  Fixed order: deterministic.
 template <int NT, int NV>
 __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const double* __restrict__ Vt, long long ld,
                                              const double* __restrict__ w, int nk, int k0, int r0, int r1) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const bool up4 = lane & 4, up2 = lane & 2, up1 = lane & 1;
   for (int c0 = 0; c0 < nk; c0 += 8) {
     double acc[8];
 #pragma unroll
@@ -681,9 +588,21 @@ __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const double* _
       for (int u = 0; u < 8; ++u)
         if (c0 + u < nk) acc[u] += Vt[(c0 + u) * ld + i] * wi;
     }
+    double a4[4], a2[2];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (c0 + u < nk) put_partial(S, k0 + c0 + u, acc[u]);
+    for (int u = 0; u < 4; ++u) {
+      const double send = up4 ? acc[u] : acc[u + 4];
+      a4[u] = (up4 ? acc[u + 4] : acc[u]) + __shfl_xor_sync(FULL, send, 4);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double send = up2 ? a4[u] : a4[u + 2];
+      a2[u] = (up2 ? a4[u + 2] : a4[u]) + __shfl_xor_sync(FULL, send, 2);
+    }
+    double a1 = (up1 ? a2[1] : a2[0]) + __shfl_xor_sync(FULL, up1 ? a2[0] : a2[1], 1);
+    a1 += __shfl_xor_sync(FULL, a1, 8);
+    a1 += __shfl_xor_sync(FULL, a1, 16);
+    if (lane < 8 && c0 + lane < nk) S.red[threadIdx.x >> 5][k0 + c0 + lane] = a1;
   }
 }
 
@@ -767,11 +686,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       PHASE(0);
       const double sj = sig[j];
       if (PC) {
-        if (A.hybrid)
-          apply_prec_hybrid<NT, TPR, D, D>(P, sid, V + j * ld, Zw, r0, r1, PT, A.h1 + K.row_off, A.h2 + K.row_off,
-                                           A.hybrid);
-        else
-          apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
+        apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);
         spmv<NT, TPR>(PT, Zw, W, r0, r1);
@@ -872,10 +787,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     if (PC) {
       for (int i = r0 + tid; i < r1; i += NT) r[i] = basis_comb(V, ld, yv, jend, i);
       cl.sync();
-      if (A.hybrid)
-        apply_prec_hybrid<NT, TPR, D, D>(P, sid, r, Zw, r0, r1, PT, A.h1 + K.row_off, A.h2 + K.row_off, A.hybrid);
-      else
-        apply_prec<D, D>(P, sid, r, Zw, r0, r1, K.nrows);
+      apply_prec<D, D>(P, sid, r, Zw, r0, r1, K.nrows);
       for (int i = r0 + tid; i < r1; i += NT) x[i] += Zw[i];
     } else {
       for (int i = r0 + tid; i < r1; i += NT) x[i] += basis_comb(V, ld, yv, jend, i);

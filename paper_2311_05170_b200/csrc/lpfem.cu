@@ -138,7 +138,6 @@ struct Family {
   // vectors
   double *base = nullptr, *z = nullptr, *lag = nullptr, *qf = nullptr, *aux = nullptr, *W = nullptr;
   double *rhs = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *V = nullptr, *ecorr = nullptr;
-  double *h1 = nullptr, *h2 = nullptr;  // hybrid preconditioner work vectors (conduit, fine)
   std::vector<KSys> hk;
   KSys* dk = nullptr;
   KStat* dstat = nullptr;
@@ -152,7 +151,7 @@ struct Family {
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
     void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, dinv, zv, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
-                    rhs, x, r, p, q, V, ecorr, dk, dstat, h1, h2};
+                    rhs, x, r, p, q, V, ecorr, dk, dstat};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
   }
@@ -407,10 +406,6 @@ void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
     F.mask = dalloc<double>(F.rows);
     F.W = dalloc<double>(F.rows);
     F.q = dalloc<double>(F.rows);
-    if (!level_family && F.level == 1) {
-      F.h1 = dalloc<double>(F.rows);
-      F.h2 = dalloc<double>(F.rows);
-    }
     if (!level_family) F.V = dalloc<double>((size_t)(GM + 1) * F.rows);
   }
   if (level_family) return;
@@ -895,9 +890,6 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
-  a.hybrid = (C.level == 1 && c->nl > 0 && getenv("LPFEM_ML_HYBRID")) ? atoi(getenv("LPFEM_ML_HYBRID")) : 0;
-  a.h1 = C.h1;
-  a.h2 = C.h2;
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
   // threshold reorthogonalised almost every iteration for identical iteration counts (cfg1-3), +20% GMRES time
   a.reorth2 = getenv("LPFEM_REORTH2") ? atof(getenv("LPFEM_REORTH2")) : 0.1;
