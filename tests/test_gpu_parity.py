@@ -98,3 +98,42 @@ def test_parity_3d_small_mms():
 def test_parity_cfg1_full_trajectory():
     worst, st = run_pair(I.config(1))
     print("cfg1 worst", worst)
+
+
+# ---- edge cases: degenerate and ragged layouts (C5, C7, C8; SURVEY 8(c) c.3 "Coarse = fine degeneracy")
+
+def test_parity_degenerate_H_equals_h():
+    """H = h: the coarse step already solves the fine equations, every correction vanishes and the composite
+    equals the coarse state (same mesh), on the GPU as in the oracle."""
+    from paper_2311_05170_b200 import LPFEM
+    cfg = I.make_config(dim=2, H=1 / 8, h=1 / 8, grid=2, dt=0.1, steps=2, problem="mms")
+    run_pair(cfg)
+    sim = LPFEM(cfg)
+    for _ in range(2):
+        sim.step()
+    comp, coarse = sim.fields(), sim.coarse_fields()
+    for f in ("pF", "pf", "pm", "u"):
+        assert np.abs(np.ravel(comp[f]) - np.ravel(coarse[f])).max() < 1e-10, f
+    sim.close()
+
+
+def test_parity_single_subdomain_per_region():
+    """One subdomain per region: the extended box is the whole region (overlap clipped at the boundary)."""
+    run_pair(I.make_config(dim=2, H=1 / 4, h=1 / 16, grid=1, dt=0.1, steps=2, problem="mms"))
+
+
+def test_parity_ragged_3x3_layout():
+    """3 x 3 subdomains: corner, edge and interior boxes of three different shapes (C7 clipping)."""
+    run_pair(I.make_config(dim=2, H=1 / 6, h=1 / 24, grid=3, dt=0.05, steps=2, problem="mms"))
+
+
+def test_parity_3d_subdomain_lag():
+    run_pair(I.make_config(dim=3, H=1 / 2, h=1 / 4, grid=2, dt=0.1, steps=2, problem="mms", lag_mode="subdomain"))
+
+
+def test_misaligned_layout_fails_loudly():
+    """Cores that do not fall on coarse grid lines are rejected (S:78 MisalignedLayout), not rounded."""
+    from paper_2311_05170_b200 import LPFEM, LPFEMError
+    cfg = I.make_config(dim=2, H=1 / 4, h=1 / 16, grid=3, dt=0.1, steps=1, problem="mms")
+    with pytest.raises(LPFEMError):
+        LPFEM(cfg)
