@@ -107,16 +107,17 @@ struct CtaPattern {
   bool sm;
 };
 
+// dyn_off: bytes of dynamic shared memory in front of the pattern (the GMRES Hessenberg matrix)
 template <int NT>
 __device__ __forceinline__ CtaPattern stage_pattern(const KArgs& A, const long long* rp, const double* val, int r0,
-                                                    int r1) {
+                                                    int r1, int dyn_off = 0) {
   extern __shared__ __align__(16) int lp_ksm[];
   CtaPattern P{rp, A.col, val, nullptr, nullptr, nullptr, A.smem_cols != 0};
   if (P.sm) {
     const long long q0 = rp[r0];
     const int nr = r1 - r0;
-    int* srp = lp_ksm;
-    int* scol = lp_ksm + ((nr + 4) & ~3);
+    int* srp = lp_ksm + dyn_off / 4;
+    int* scol = srp + ((nr + 4) & ~3);
     for (int i = threadIdx.x; i <= nr; i += NT) srp[i] = (int)(rp[r0 + i] - q0);
     const long long nq = rp[r1] - q0;
     for (long long i = threadIdx.x; i < nq; i += NT) scol[i] = A.col[q0 + i];
@@ -255,6 +256,9 @@ __device__ __forceinline__ void spmv(const CtaPattern& P, const double* __restri
   else
     spmv_rows<NT, TPR>(P.rp, P.col, P.val, x, y, r0, r1);
 }
+
+// bytes of the GMRES(M) Hessenberg matrix (M + 1) x M in dynamic shared memory, 16-byte aligned
+__host__ __device__ constexpr int gmres_h_bytes(int M) { return (((M + 1) * M * 8) + 15) & ~15; }
 
 // ---------------------------------------------------------------------------------------------
 template <int NT, int TPR>
@@ -647,9 +651,12 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   double* Zw = PC ? A.q + K.row_off : nullptr;
   const long long ld = A.rows_total;
   double* V = A.V + K.row_off;
-  const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1);
+  // Hessenberg matrix in dynamic shared memory (static shared memory is capped at 48 KB), pattern after it
+  extern __shared__ __align__(16) double lp_gdyn[];
+  double(*H)[M] = reinterpret_cast<double(*)[M]>(lp_gdyn);
+  const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1, gmres_h_bytes(M));
   __shared__ RedSmem<NT, M + 2> S;
-  __shared__ double H[M + 1][M], cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1], sig[M + 1], hs[M + 1];
+  __shared__ double cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1], sig[M + 1], hs[M + 1];
   int par = 0;
   const int tid = threadIdx.x;
 #ifdef LPFEM_PHASE_TIMERS

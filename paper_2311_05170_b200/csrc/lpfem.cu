@@ -683,11 +683,11 @@ void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Arg
 // largest (row offsets + column indices) of any CTA's row block, or 0 when one does not fit next to the
 // kernel's static shared memory (the kernels then read the pattern from global memory).
 template <class Kern>
-size_t pattern_smem(Kern k, const Family& F, int CL) {
+size_t pattern_smem(Kern k, const Family& F, int CL, size_t front = 0) {
   if (getenv("LPFEM_NO_SMEM_PATTERN") || F.hrp.empty()) return 0;
   cudaFuncAttributes at;
   CK(cudaFuncGetAttributes(&at, k));
-  const long long budget = 227LL * 1024 - (long long)at.sharedSizeBytes - 1024;
+  const long long budget = 227LL * 1024 - (long long)at.sharedSizeBytes - (long long)front - 1024;
   long long need = 0;
   for (const KSys& K : F.hk) {
     const int chunk = (K.nrows + CL - 1) / CL;
@@ -903,14 +903,15 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
 #endif
   const bool pc = C.level == 1 && c->nl > 0;
 
+  const size_t hb = gmres_h_bytes(GM);
   auto go = [&](auto k) {
     if (!C.cluster_checked && !C.bandwidth_bound) {
-      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, pattern_smem(k, C, C.cluster));
+      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb));
       C.cluster_checked = true;
     }
-    const size_t sm = pattern_smem(k, C, C.cluster);
+    const size_t sm = pattern_smem(k, C, C.cluster, hb);
     a.smem_cols = sm > 0;
-    launch_cluster_sm(k, (int)C.hk.size(), C.cluster, NTG, sm, c->st, a, c->ml);
+    launch_cluster_sm(k, (int)C.hk.size(), C.cluster, NTG, hb + sm, c->st, a, c->ml);
   };
   if (pc) {
     if (D == 2)
@@ -957,8 +958,9 @@ void decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
   Family& C = c->fam[1][1];
   Family& P = c->fam[1][0];
   if (!C.hk.empty() && !C.cluster_checked && !C.bandwidth_bound) {
+    const size_t hb = gmres_h_bytes(GM);
     auto chk = [&](auto k) {
-      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, pattern_smem(k, C, C.cluster));
+      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb));
       C.cluster_checked = true;
     };
     const bool pc = c->nl > 0;
