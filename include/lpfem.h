@@ -161,6 +161,17 @@ lpfem_status lpfem_get_stats(const lpfem_ctx* ctx, lpfem_stats* out);
 lpfem_status lpfem_get_system(lpfem_ctx* ctx, int family, int local_index, int field, long long* nrows,
                               long long* nnz, long long* rowptr, int* col, double* val, double* rhs, double* x);
 
+/* Measurement of the sparse matrix-vector product the Krylov kernels are built from (BASELINE metric
+ * "SpMV % HBM peak"): y = A x over every fine system of one family (family 0 porous, the
+ * three fields; 1 conduit, the current Oseen operators), with the same device routine (krylov.cuh
+ * spmv_rows, same lanes per row) launched over all rows, `reps` times on the ctx stream; if flush != 0 a
+ * 512 MiB buffer is written before every rep so each rep streams the matrix from HBM.  Returns the mean
+ * device time per rep (CUDA events around the SpMV launch only) and the algorithmic bytes per rep:
+ * 12 per nonzero (fp64 value + int32 column) + 8 per row pointer + 16 per row (x once, y).  Does not
+ * change the solution state (reads the RHS vector, writes a Krylov work vector).  Host pointers. */
+lpfem_status lpfem_bench_spmv(lpfem_ctx* ctx, int family, int reps, int flush, double* ms_per_rep,
+                              double* bytes_per_rep);
+
 /* Multi-GPU plan (host only, no device needed): subdomain positions are split into contiguous
  * blocks over `world` ranks; a fine node belongs to the rank of its owning subdomain (C3).  For one region
  * meshed with n_cells fine cells per axis, returns global node indices (P2 half-grid lexicographic, or P1

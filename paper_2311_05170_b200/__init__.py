@@ -29,7 +29,7 @@ STATUS = ["ok", "einval", "enotdiv", "emisalign", "enoconv", "ecuda", "enccl", "
 # Exported symbols (kept in sync with include/lpfem.h; checked by tests/test_abi.py)
 SYMBOLS = ["lpfem_nccl_unique_id", "lpfem_create", "lpfem_step", "lpfem_get_sizes", "lpfem_get_fields",
            "lpfem_get_coarse_fields", "lpfem_get_mesh", "lpfem_get_layout", "lpfem_get_stats", "lpfem_get_system",
-           "lpfem_halo_plan", "lpfem_last_error", "lpfem_status_string", "lpfem_destroy"]
+           "lpfem_halo_plan", "lpfem_last_error", "lpfem_status_string", "lpfem_destroy", "lpfem_bench_spmv"]
 
 
 class Geometry(C.Structure):
@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
         L.lpfem_get_mesh.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, P(C.c_longlong)]
         L.lpfem_get_layout.argtypes = [C.c_void_p] + [C.c_void_p] * 6 + [P(C.c_int)]
         L.lpfem_get_stats.argtypes = [C.c_void_p, P(Stats)]
+        L.lpfem_bench_spmv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]
         L.lpfem_get_system.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, P(C.c_longlong), P(C.c_longlong),
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.lpfem_last_error.argtypes = [C.c_void_p]
@@ -212,6 +213,12 @@ class LPFEM:
                         "core0": tuple(arrs[0][3 * i:3 * i + self.d]), "core1": tuple(arrs[1][3 * i:3 * i + self.d]),
                         "box0": tuple(arrs[2][3 * i:3 * i + self.d]), "box1": tuple(arrs[3][3 * i:3 * i + self.d])})
         return out
+
+    def bench_spmv(self, family: int = 1, reps: int = 10, flush: bool = True) -> dict:
+        """lpfem_bench_spmv: mean device ms and algorithmic bytes of one batched SpMV over a family."""
+        ms, b = C.c_double(), C.c_double()
+        self._check(lib().lpfem_bench_spmv(self._h, family, reps, int(flush), C.byref(ms), C.byref(b)))
+        return {"ms": ms.value, "bytes": b.value, "gbs": b.value / (ms.value * 1e-3) / 1e9}
 
     def stats(self) -> dict:
         s = Stats()

@@ -195,23 +195,124 @@ __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, cons
     double s = 0.0;
     if (r < r1) {
       const long long qb = rp[r], qe = rp[r + 1];
+      // Loads are unconditional, the index clamped to the row's last entry (an L1 hit) and its weight zeroed:
+      // with predicated loads the compiler chained col -> x -> FMA one entry at a time (2-3 loads in flight per
+      // thread, measured 3 TB/s on cfg4); unconditional loads let all 3U loads of a batch issue back to back.
       for (long long q0 = qb + lane; q0 < qe; q0 += (long long)TPR * U) {
         int cc[U];
-        double vv[U];
+        double vv[U], xx[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const long long q = q0 + (long long)u * TPR;
-          const bool in = q < qe;
-          cc[u] = in ? __ldg(col + q) : 0;
-          vv[u] = in ? __ldg(val + q) : 0.0;
+          const long long q = min(q0 + (long long)u * TPR, qe - 1);
+          cc[u] = __ldg(col + q);
+          vv[u] = __ldg(val + q);
         }
+        // a warp barrier between the (col, val) loads and the x gathers keeps the compiler from interleaving
+        // them (it otherwise schedules for 32 registers and chains col -> x per entry)
+        __syncwarp(__activemask());
 #pragma unroll
-        for (int u = 0; u < U; ++u) s += vv[u] * x[cc[u]];
+        for (int u = 0; u < U; ++u) xx[u] = x[cc[u]];
+        // zero the weights of clamped entries, then a pairwise tree (independent products, short chain)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (q0 + (long long)u * TPR >= qe) vv[u] = 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) vv[u] *= xx[u];
+#pragma unroll
+        for (int w = U / 2; w > 0; w >>= 1)
+#pragma unroll
+          for (int u = 0; u < w; ++u) vv[u] += vv[u + w];
+        s += vv[0];
       }
     }
 #pragma unroll
     for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
     if (r < r1 && lane == 0) y[r] = s;
+  }
+}
+
+// Software-pipelined variant: while the x gathers of row r are in flight, the (col, val) batch of row r + NG and
+// the row pointers of row r + 2 NG are already loading (three stages), so the loads of a thread never wait on
+// one another; rows longer than TPR * U finish their extra batches inline.  Same sums as spmv_rows per batch.
+template <int NT, int TPR, int U>
+__device__ __forceinline__ void spmv_rows_pipe(const long long* __restrict__ rp, const int* __restrict__ col,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               double* __restrict__ y, int r0, int r1) {
+  constexpr int NG = NT / TPR;
+  const int lane = threadIdx.x % TPR;
+  int r = r0 + threadIdx.x / TPR;
+  auto rowq = [&](int rr, long long& b, long long& e) {
+    if (rr < r1) {
+      b = rp[rr];
+      e = rp[rr + 1];
+    } else {
+      b = 0;
+      e = 0;
+    }
+  };
+  auto load = [&](long long q0, long long e, int* cc, double* vv) {
+    if (q0 - lane < e) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long q = min(q0 + (long long)u * TPR, e - 1);
+        cc[u] = __ldg(col + q);
+        vv[u] = __ldg(val + q);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        cc[u] = 0;
+        vv[u] = 0.0;
+      }
+    }
+  };
+  auto batch = [&](long long q0, long long e, const int* cc, double* vv) {
+    double xx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xx[u] = x[cc[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u) vv[u] = q0 + (long long)u * TPR < e ? vv[u] * xx[u] : 0.0;
+#pragma unroll
+    for (int w = U / 2; w > 0; w >>= 1)
+#pragma unroll
+      for (int u = 0; u < w; ++u) vv[u] += vv[u + w];
+    return vv[0];
+  };
+  long long b0, e0, b1, e1;
+  rowq(r, b0, e0);
+  rowq(r + NG, b1, e1);
+  int cc[U];
+  double vv[U];
+  load(b0 + lane, e0, cc, vv);
+  for (int base = r0; base < r1; base += NG) {
+    long long b2, e2;
+    rowq(r + 2 * NG, b2, e2);
+    int cn[U];
+    double vn[U];
+    load(b1 + lane, e1, cn, vn);
+    double s = 0.0;
+    if (b0 < e0) {
+      s = batch(b0 + lane, e0, cc, vv);
+      for (long long q0 = b0 + lane + (long long)TPR * U; q0 < e0; q0 += (long long)TPR * U) {
+        int c2[U];
+        double v2[U];
+        load(q0, e0, c2, v2);
+        s += batch(q0, e0, c2, v2);
+      }
+    }
+#pragma unroll
+    for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
+    if (r < r1 && lane == 0) y[r] = s;
+    r += NG;
+    b0 = b1;
+    e0 = e1;
+    b1 = b2;
+    e1 = e2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cc[u] = cn[u];
+      vv[u] = vn[u];
+    }
   }
 }
 
@@ -233,13 +334,13 @@ __device__ __forceinline__ void spmv_rows_sm(const int* __restrict__ srp, const 
         double vv[U], xx[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int q = q0 + u * TPR;
-          const bool in = q < qe;
-          vv[u] = in ? __ldg(sval + q) : 0.0;
-          xx[u] = in ? x[scol[q]] : 0.0;
+          const int q = min(q0 + u * TPR, qe - 1);  // unconditional loads (see spmv_rows)
+          vv[u] = __ldg(sval + q);
+          xx[u] = x[scol[q]];
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) s += vv[u] * xx[u];
+        for (int u = 0; u < U; ++u)
+          if (q0 + u * TPR < qe) s += vv[u] * xx[u];
       }
     }
 #pragma unroll
@@ -248,17 +349,39 @@ __device__ __forceinline__ void spmv_rows_sm(const int* __restrict__ srp, const 
   }
 }
 
-template <int NT, int TPR>
+// PIPE: software-pipelined rows (measured better for the porous PCG and the 2D conduit GMRES: cfg4 PCG 321 -> 278
+// ms, cfg2 GMRES 167 -> 164 ms; worse for the 3D conduit GMRES: cfg3 99 -> 107 ms)
+template <int NT, int TPR, bool PIPE = true>
 __device__ __forceinline__ void spmv(const CtaPattern& P, const double* __restrict__ x, double* __restrict__ y, int r0,
                                      int r1) {
   if (P.sm)
     spmv_rows_sm<NT, TPR>(P.srp, P.scol, P.sval, x, y, r0, r1);
+  else if (PIPE)
+    spmv_rows_pipe<NT, TPR, 4>(P.rp, P.col, P.val, x, y, r0, r1);
   else
     spmv_rows<NT, TPR>(P.rp, P.col, P.val, x, y, r0, r1);
 }
 
 // bytes of the GMRES(M) Hessenberg matrix (M + 1) x M in dynamic shared memory, 16-byte aligned
 __host__ __device__ constexpr int gmres_h_bytes(int M) { return (((M + 1) * M * 8) + 15) & ~15; }
+
+// Standalone batched SpMV over every system of a family (lpfem_bench_spmv): the Krylov kernels' row routine,
+// grid (row blocks, systems).
+template <int NT, int TPR, int PIPE_U>
+__global__ void __launch_bounds__(NT) k_spmv_family(const KSys* __restrict__ sys, const long long* __restrict__ rowptr,
+                                                    const int* __restrict__ col, const double* __restrict__ val,
+                                                    const double* __restrict__ x, double* __restrict__ y,
+                                                    int rows_per_cta) {
+  const KSys K = sys[blockIdx.y];
+  const int r0 = blockIdx.x * rows_per_cta;
+  if (r0 >= K.nrows) return;
+  const int r1 = min(K.nrows, r0 + rows_per_cta);
+  if (PIPE_U > 0)
+    spmv_rows_pipe<NT, TPR, (PIPE_U > 0 ? PIPE_U : 1)>(rowptr + K.prow_off, col, val + K.val_off, x + K.row_off,
+                                                      y + K.row_off, r0, r1);
+  else
+    spmv_rows<NT, TPR>(rowptr + K.prow_off, col, val + K.val_off, x + K.row_off, y + K.row_off, r0, r1);
+}
 
 // ---------------------------------------------------------------------------------------------
 template <int NT, int TPR>
@@ -696,9 +819,9 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);
-        spmv<NT, TPR>(PT, Zw, W, r0, r1);
+        spmv<NT, TPR, D == 2>(PT, Zw, W, r0, r1);
       } else {
-        spmv<NT, TPR>(PT, V + j * ld, W, r0, r1);
+        spmv<NT, TPR, D == 2>(PT, V + j * ld, W, r0, r1);
       }
       __syncthreads();
       PHASE(2);
@@ -801,7 +924,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     }
     cl.sync();
     ++nspmv;
-    spmv<NT, TPR>(PT, x, W, r0, r1);
+    spmv<NT, TPR, D == 2>(PT, x, W, r0, r1);
     __syncthreads();
     double pr = 0.0;
     for (int i = r0 + tid; i < r1; i += NT) {

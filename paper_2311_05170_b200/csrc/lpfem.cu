@@ -68,7 +68,7 @@ T* dalloc(size_t n) {
 #define LPFEM_TPR2 4
 #endif
 #ifndef LPFEM_TPR3
-#define LPFEM_TPR3 16
+#define LPFEM_TPR3 8
 #endif
 // GMRES restart length (compile-time: shared-memory Hessenberg and reductions).  Measured (cfg1/2/3 max
 // iterations 316/344/484 at 30 -> 246/313/399 at 45; GMRES time -1%/-10%/-14%)
@@ -77,7 +77,8 @@ constexpr int GM = LPFEM_GM;
 #define LPFEM_NTG 1024
 #endif
 constexpr int NTG = LPFEM_NTG;  // threads per CTA of the conduit GMRES
-constexpr int TPR2 = LPFEM_TPR2, TPR3 = LPFEM_TPR3;  // conduit SpMV lanes per row (2D ~28 nnz/row, 3D ~93)
+constexpr int TPR2 = LPFEM_TPR2, TPR3 = LPFEM_TPR3;  // conduit SpMV lanes per row (2D ~28 nnz/row, 3D ~93; 3D 8 vs 16:
+                                                     // cfg4 GMRES 2169 -> 2145 ms)
 
 // NCCL is loaded lazily (multi-GPU only) so that the library has no link-time NCCL dependency; in a torch
 // process this resolves to the NCCL torch already loaded.
@@ -2224,6 +2225,76 @@ lpfem_status lpfem_get_system(lpfem_ctx* c, int family, int local_index, int fie
     return LPFEM_ECUDA;
   if (x && cudaMemcpy(x, F.x + roff, S.nrows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) return LPFEM_ECUDA;
   return LPFEM_OK;
+}
+
+lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, double* ms_per_rep,
+                              double* bytes_per_rep) {
+  if (!c || family < 0 || family > 1 || reps < 1 || !ms_per_rep || !bytes_per_rep) return LPFEM_EINVAL;
+  try {
+    CK(cudaSetDevice(c->dist.device));
+    Family& F = c->fam[1][family];
+    if (F.hk.empty() || F.nnz == 0) throw Err(LPFEM_ESTATE, "family has no systems on this rank");
+    const double* val = family == 0 ? F.val : F.aout;
+    const double* x = F.rhs;
+    double* y = family == 0 ? F.q : F.W;
+    constexpr int NT = 512;
+    int tpr = family == 0 ? (c->D == 2 ? 4 : 8) : (c->D == 2 ? TPR2 : TPR3);
+    if (getenv("LPFEM_SPMV_TPR")) tpr = atoi(getenv("LPFEM_SPMV_TPR"));  // experiment
+    const int rpc = 4 * NT / tpr;
+    int maxr = 0;
+    double bytes = 0.0;
+    for (size_t i = 0; i < F.hk.size(); ++i) {
+      const KSys& K = F.hk[i];
+      maxr = std::max(maxr, K.nrows);
+      const double nz = (double)(F.hrp[K.prow_off + K.nrows] - F.hrp[K.prow_off]);
+      bytes += 12.0 * nz + 8.0 * (K.nrows + 1) + 16.0 * K.nrows;
+    }
+    const dim3 grid((maxr + rpc - 1) / rpc, (unsigned)F.hk.size());
+    void* fb = nullptr;
+    const size_t fbytes = 512u << 20;
+    if (flush) CK(cudaMalloc(&fb, fbytes));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double tot = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      if (flush) CK(cudaMemsetAsync(fb, r & 0xff, fbytes, c->st));
+      CK(cudaEventRecord(e0, c->st));
+      // the Krylov kernels' choice: pipelined rows (U = 4) for the porous family and the 2D conduit, plain 3D conduit
+      const int pu = getenv("LPFEM_SPMV_PIPE") ? atoi(getenv("LPFEM_SPMV_PIPE")) : (family == 0 || c->D == 2 ? 4 : 0);
+#define LP_SPMV(T, P) k_spmv_family<NT, T, P><<<grid, NT, 0, c->st>>>(F.dk, F.rowptr, F.col, val, x, y, rpc)
+      if (pu == 4) {
+        if (tpr == 4) LP_SPMV(4, 4);
+        else if (tpr == 8) LP_SPMV(8, 4);
+        else if (tpr == 16) LP_SPMV(16, 4);
+        else LP_SPMV(32, 4);
+      } else if (pu == 8) {
+        if (tpr == 4) LP_SPMV(4, 8);
+        else if (tpr == 8) LP_SPMV(8, 8);
+        else if (tpr == 16) LP_SPMV(16, 8);
+        else LP_SPMV(32, 8);
+      } else {
+        if (tpr == 4) LP_SPMV(4, 0);
+        else if (tpr == 8) LP_SPMV(8, 0);
+        else LP_SPMV(16, 0);
+      }
+#undef LP_SPMV
+      CKL();
+      CK(cudaEventRecord(e1, c->st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.0f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      tot += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (fb) cudaFree(fb);
+    *ms_per_rep = tot / reps;
+    *bytes_per_rep = bytes;
+    return LPFEM_OK;
+  } catch (const Err& e) {
+    return fail(c, e);
+  }
 }
 
 lpfem_status lpfem_halo_plan(int dim, const int n_cells[3], const int subdomain_grid[3], int overlap_cells, int rank,
