@@ -239,6 +239,8 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
   int base[3] = {0, 0, 0};
   for (int a = 0; a < D; ++a) base[a] = q * l[a];
   double s0 = 0.0;
+  // unconditional gathers: points outside the box are clamped onto it and weighted 0 (predicated loads were
+  // chained one stencil entry at a time by the compiler)
 #pragma unroll 4
   for (int i = b + lane; valid && i < e; i += LN) {
     int g0[3];
@@ -246,9 +248,10 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
     for (int a = 0; a < D; ++a) {
       g0[a] = base[a] + T->off[i][a];
       ok0 = ok0 && g0[a] >= 0 && g0[a] <= 2 * SF.nc[a];
-      g0[a] >>= sh;
+      g0[a] = min(max(g0[a], 0), 2 * SF.nc[a]) >> sh;
     }
-    if (ok0) s0 += T->w[i] * sv[lex<D>(g0, shp)];
+    const double v = sv[lex<D>(g0, shp)];
+    s0 += ok0 ? T->w[i] * v : 0.0;
   }
 #pragma unroll
   for (int o = LN / 2; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o, LN);
@@ -268,14 +271,18 @@ __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& 
     int code[n2_of(D)];
     double w[n2_of(D)];
     p2_weights<D>(g, q, SC.nc, cell, code, w);
+    // unconditional gathers (every code lies in the coarse cell); zero weights add nothing
+    double v[n2_of(D)];
 #pragma unroll
     for (int n = 0; n < n2_of(D); ++n) {
-      if (w[n] == 0.0) continue;
       int l[3];
       code_point<D>(code[n], cell, l);
       const long long id = (long long)k * SC.n2 + lex<D>(l, SC.np);
-      s += w[n] * (scl ? scl[id] * src[id] : src[id]);
+      v[n] = scl ? scl[id] * src[id] : src[id];
     }
+#pragma unroll
+    for (int n = 0; n < n2_of(D); ++n)
+      if (w[n] != 0.0) s += w[n] * v[n];
   } else {
     const int shpf[3] = {SF.nc[0] + 1, SF.nc[1] + 1, SF.nc[2] + 1};
     unlex<D>(row - NC * SF.n2, shpf, g);
@@ -284,15 +291,18 @@ __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& 
     double w[D + 1];
     p1_weights<D>(g, q, SC.nc, cell, code, w);
     const int shpc[3] = {SC.nc[0] + 1, SC.nc[1] + 1, SC.nc[2] + 1};
+    double v[D + 1];
 #pragma unroll
     for (int n = 0; n <= D; ++n) {
-      if (w[n] == 0.0) continue;
       int l[3];
       code_point<D>(code[n], cell, l);
       for (int a = 0; a < D; ++a) l[a] >>= 1;
       const long long id = (long long)NC * SC.n2 + lex<D>(l, shpc);
-      s += w[n] * (scl ? scl[id] * src[id] : src[id]);
+      v[n] = scl ? scl[id] * src[id] : src[id];
     }
+#pragma unroll
+    for (int n = 0; n <= D; ++n)
+      if (w[n] != 0.0) s += w[n] * v[n];
   }
   return s;
 }
