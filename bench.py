@@ -264,11 +264,14 @@ def main():
     }
     # SpMV building block of the Krylov kernels (BASELINE metric "SpMV % HBM peak"): the conduit family's batched
     # y = A x with the same device routine, L2 flushed before every rep, outside the timed region
-    sp = sim.bench_spmv(1, reps=10, flush=True)
-    out["spmv"] = {"family": "conduit (fine Oseen operators, all local systems)", "bound": "hbm",
-                   "achieved": sp["gbs"], "peak": peak, "unit": "GB/s", "frac": sp["gbs"] / peak,
-                   "ms_per_rep": sp["ms"], "algorithmic_bytes_per_rep": sp["bytes"],
-                   "l2": "flushed before every rep"}
+    try:
+        sp = sim.bench_spmv(1, reps=10, flush=True)
+        out["spmv"] = {"family": "conduit (fine Oseen operators, all systems of rank 0)", "bound": "hbm",
+                       "achieved": sp["gbs"], "peak": peak, "unit": "GB/s", "frac": sp["gbs"] / peak,
+                       "ms_per_rep": sp["ms"], "algorithmic_bytes_per_rep": sp["bytes"],
+                       "l2": "flushed before every rep"}
+    except Exception as e:  # a rank without conduit systems (small configs on many GPUs)
+        out["spmv"] = {"unavailable": str(e)[:120]}
     sim.close()
     # end to end through the public API with host buffers: create from host inputs, K steps, fields -> host
     if not args.no_e2e:
