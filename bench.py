@@ -263,7 +263,8 @@ def main():
         "fine_value": D * args.steps / ((st1["t_fine_ms"] - st0["t_fine_ms"]) * 1e-3),
     }
     # SpMV building block of the Krylov kernels (BASELINE metric "SpMV % HBM peak"): the conduit family's batched
-    # y = A x with the same device routine, L2 flushed before every rep, outside the timed region
+    # y = A x with the same device routine, L2 flushed before every rep, outside the timed region (measured on
+    # the bench context before it closes; the e2e run below creates its own context)
     try:
         sp = sim.bench_spmv(1, reps=10, flush=True)
         out["spmv"] = {"family": "conduit (fine Oseen operators, all systems of rank 0)", "bound": "hbm",
@@ -273,6 +274,8 @@ def main():
     except Exception as e:  # a rank without conduit systems (small configs on many GPUs)
         out["spmv"] = {"unavailable": str(e)[:120]}
     sim.close()
+    del flush
+    torch.cuda.empty_cache()
     # end to end through the public API with host buffers: create from host inputs, K steps, fields -> host
     if not args.no_e2e:
         torch.cuda.synchronize()

@@ -92,6 +92,7 @@ struct KArgs {
   long long* phase;  // LPFEM_PHASE_TIMERS only
   double reorth2;    // GMRES: reorthogonalise when ||w'||^2 < reorth2 ||w||^2 (Kahan-Parlett: 0.5)
   int smem_cols;     // 1: every CTA stages its rows' pattern (row offsets + column indices) in shared memory
+  int warm;          // 1: x holds the previous step's solution of the same system, used as the initial guess
 };
 
 // Sparsity pattern of the CTA's rows [r0, r1): staged once per solve in dynamic shared memory when it fits (the
@@ -621,7 +622,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
   double pw = 0.0;
   for (int i = r0 + tid; i < r1; i += NT) {
     const double bi = b[i];
-    x[i] = 0.0;
+    if (!A.warm) x[i] = 0.0;
     r[i] = bi;
     pw += w[i] * bi * bi;
   }
@@ -632,7 +633,25 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
   int it = 0, conv = 0, nspmv = 0, checks = 0;
   double relres = 0.0, rz = 0.0;
   bool fresh = true;  // p must be restarted from z
-  if (bnorm == 0.0) conv = 1;
+  if (bnorm == 0.0) {
+    conv = 1;
+    for (int i = r0 + tid; i < r1; i += NT) x[i] = 0.0;
+  } else if (A.warm) {
+    // initial guess: the previous step's correction (the stopping test stays ||b - A x|| <= rtol ||b||, C19)
+    spmv<NT, TPR>(PT, x, q, r0, r1);
+    __syncthreads();
+    double pt = 0.0;
+    for (int i = r0 + tid; i < r1; i += NT) {
+      const double ri = b[i] - q[i];
+      r[i] = ri;
+      pt += w[i] * ri * ri;
+    }
+    put_partial(S, 0, pt);
+    cluster_sum(S, 1, par);
+    ++nspmv;
+    relres = sqrt(S.fin[0]) / bnorm;
+    if (S.fin[0] <= tol2) conv = 1;
+  }
   while (!conv) {
     // z = M^-1 r, rz = r . z
     cl.sync();
@@ -789,7 +808,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   double pb = 0.0;
   for (int i = r0 + tid; i < r1; i += NT) {
     const double bi = b[i];
-    x[i] = 0.0;
+    if (!A.warm) x[i] = 0.0;
     r[i] = bi;
     pb += bi * bi;
   }
@@ -800,7 +819,25 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   const double tol = A.rtol * bnorm;
   int it = 0, conv = 0, nspmv = 0;
   long long vsum = 0;
-  if (bnorm == 0.0) conv = 1;
+  if (bnorm == 0.0) {
+    conv = 1;
+    for (int i = r0 + tid; i < r1; i += NT) x[i] = 0.0;
+  } else if (A.warm) {
+    // initial guess: the previous step's correction (the stopping test stays ||b - A x|| <= rtol ||b||, C19)
+    spmv<NT, TPR, D == 2>(PT, x, W, r0, r1);
+    __syncthreads();
+    double pr = 0.0;
+    for (int i = r0 + tid; i < r1; i += NT) {
+      const double ri = b[i] - W[i];
+      r[i] = ri;
+      pr += ri * ri;
+    }
+    put_partial(S, 0, pr);
+    cluster_sum(S, 1, par);
+    ++nspmv;
+    beta = sqrt(S.fin[0]);
+    if (beta <= tol) conv = 1;
+  }
   while (!conv) {
     for (int i = r0 + tid; i < r1; i += NT) V[i] = r[i];
     if (tid == 0) {
