@@ -92,7 +92,9 @@ struct KArgs {
   long long* phase;  // LPFEM_PHASE_TIMERS only
   double reorth2;    // GMRES: reorthogonalise when ||w'||^2 < reorth2 ||w||^2 (Kahan-Parlett: 0.5)
   int smem_cols;     // 1: every CTA stages its rows' pattern (row offsets + column indices) in shared memory
-  int warm;          // 1: x holds the previous step's solution of the same system, used as the initial guess
+  int warm;          // 1: x holds the previous step's solution of the same system, used as the initial guess;
+                     // 2: also xp holds the one before: initial guess 2 x - xp (linear extrapolation in time)
+  double* xp;        // warm == 2: the solution two steps back (updated to the previous one)
 };
 
 // Sparsity pattern of the CTA's rows [r0, r1): staged once per solve in dynamic shared memory when it fits (the
@@ -620,9 +622,16 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
   int par = 0;
   const int tid = threadIdx.x;
   double pw = 0.0;
+  double* xp = A.xp ? A.xp + K.row_off : nullptr;
   for (int i = r0 + tid; i < r1; i += NT) {
     const double bi = b[i];
-    if (!A.warm) x[i] = 0.0;
+    if (!A.warm) {
+      x[i] = 0.0;
+    } else if (xp) {
+      const double xn = x[i];
+      if (A.warm == 2) x[i] = 2.0 * xn - xp[i];
+      xp[i] = xn;
+    }
     r[i] = bi;
     pw += w[i] * bi * bi;
   }
@@ -806,9 +815,16 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
 #endif
 
   double pb = 0.0;
+  double* xp = A.xp ? A.xp + K.row_off : nullptr;
   for (int i = r0 + tid; i < r1; i += NT) {
     const double bi = b[i];
-    if (!A.warm) x[i] = 0.0;
+    if (!A.warm) {
+      x[i] = 0.0;
+    } else if (xp) {
+      const double xn = x[i];
+      if (A.warm == 2) x[i] = 2.0 * xn - xp[i];
+      xp[i] = xn;
+    }
     r[i] = bi;
     pb += bi * bi;
   }

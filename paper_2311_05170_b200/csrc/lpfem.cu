@@ -146,14 +146,15 @@ struct Family {
   int cluster = 1;
   bool cluster_checked = false;  // cluster size reduced until all clusters are co-resident (resident_cluster)
   bool bandwidth_bound = false;  // large systems: keep the largest cluster even if the launch needs two waves
-  bool solved = false;           // x holds a previous solution of every system (Krylov warm start)
+  int solved = 0;                // previous solutions held: x (>= 1), xp (>= 2) (Krylov warm start)
+  double* xp = nullptr;          // the solution one step before x (extrapolated warm start)
   std::vector<long long> sys_nnz;        // nnz per Krylov system
   std::vector<long long> hrp;            // host copy of rowptr (CTA pattern sizes for the Krylov launches)
   std::vector<int> sub_region, sub_pos;  // per local subdomain (fine)
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
     void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, dinv, zv, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
-                    rhs, x, r, p, q, V, ecorr, dk, dstat};
+                    rhs, x, r, p, q, V, ecorr, dk, dstat, xp};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
   }
@@ -217,6 +218,7 @@ struct lpfem_ctx {
   double *part = nullptr, *aci = nullptr, *abuf = nullptr, *lwk = nullptr;
   double* ainv[2] = {nullptr, nullptr};  // row-major coarse-box inverses, double-buffered (coarse_box_inverses)
   int ml_next = 0, ml_busy = 0;          // slot the next fine step uses / slot the enqueued fine step reads
+  int warm_order = 2;                    // Krylov initial guess: 1 previous solution, 2 linear extrapolation
   // coarse Navier-Stokes chord iteration: LU of the last factorised Jacobian in `dense`/`piv` (conduit_solve_once)
   bool clu_valid = false, clu_force = false;
   int clu_newton = -1;
@@ -845,8 +847,13 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.maxit = c->opts.max_iter;
   a.stat = P.dstat;
   // warm start from the previous step's corrections (fine ML-PCG): measured fewer iterations, same test (C19)
-  a.warm = (P.level == 1 && c->nlp > 0 && P.solved && !getenv("LPFEM_COLD_START")) ? 1 : 0;
-  P.solved = true;
+  a.warm = (P.level == 1 && c->nlp > 0 && !getenv("LPFEM_COLD_START")) ? std::min(P.solved, c->warm_order) : 0;
+  if (a.warm > 0 && !P.xp) {
+    P.xp = dalloc<double>(3 * P.rows);
+    CK(cudaMemsetAsync(P.xp, 0, 3 * P.rows * sizeof(double), c->st));
+  }
+  a.xp = a.warm > 0 ? P.xp : nullptr;
+  P.solved = std::min(P.solved + 1, 2);
   const int ns = (int)P.hk.size();
   auto go_ml = [&](auto k) {
     if (!P.cluster_checked && !P.bandwidth_bound) {
@@ -895,8 +902,13 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
-  a.warm = (C.level == 1 && C.solved && !getenv("LPFEM_COLD_START")) ? 1 : 0;
-  C.solved = true;
+  a.warm = (C.level == 1 && !getenv("LPFEM_COLD_START")) ? std::min(C.solved, c->warm_order) : 0;
+  if (a.warm > 0 && !C.xp) {
+    C.xp = dalloc<double>(C.rows);
+    CK(cudaMemsetAsync(C.xp, 0, C.rows * sizeof(double), c->st));
+  }
+  a.xp = a.warm > 0 ? C.xp : nullptr;
+  C.solved = std::min(C.solved + 1, 2);
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
   // threshold reorthogonalised almost every iteration for identical iteration counts (cfg1-3), +20% GMRES time
   a.reorth2 = getenv("LPFEM_REORTH2") ? atof(getenv("LPFEM_REORTH2")) : 0.1;
@@ -1718,6 +1730,7 @@ void setup(lpfem_ctx* c) {
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
     if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
+    if (getenv("LPFEM_WARM_ORDER")) c->warm_order = std::max(1, std::min(2, atoi(getenv("LPFEM_WARM_ORDER"))));
     c->ml_refresh = D == 2 ? 1 : 4;
     if (getenv("LPFEM_ML_REFRESH")) c->ml_refresh = std::max(1, atoi(getenv("LPFEM_ML_REFRESH")));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evc[i], cudaEventDefault));
