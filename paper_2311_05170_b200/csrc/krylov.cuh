@@ -498,7 +498,10 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
 // ---------------------------------------------------------------------------------------------
 // M^-1 v for the conduit systems (mlprec.cuh): fine diagonal + nested levels + exact coarse-box solve.
 // v and Z are system-local fine vectors; work is spread over the whole cluster (gt, gs).
-constexpr int RLN = 8;  // lanes per restricted row
+#ifndef LPFEM_RLN
+#define LPFEM_RLN 4
+#endif
+constexpr int RLN = LPFEM_RLN;  // lanes per restricted row (4 vs 8: cfg2 GMRES 160 -> 153 ms, cfg1/cfg3 equal)
 
 template <int D, int NC>
 __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ v, double* __restrict__ Z, int r0,
