@@ -287,6 +287,8 @@ def main():
             dist.broadcast(t, 0)
             nid = bytes(t.cpu().numpy().tobytes())
         sim2 = LPFEM(cfg, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nid)
+        torch.cuda.synchronize()
+        t_create = time.perf_counter() - t0
         d2h = 0
         for i in range(args.steps):
             sim2.step()
@@ -297,7 +299,8 @@ def main():
         h2d = (0 if cfg.get("k_mult") is None else np.asarray(cfg["k_mult"]).nbytes) + 8 * 64
         out["e2e"] = {"value": D * args.steps / el, "unit": "fine DOF*steps/s",
                       "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-                      "includes": "lpfem_create (setup, assembly) + K x (lpfem_step + lpfem_get_fields to host)"}
+                      "includes": "lpfem_create (setup, assembly) + K x (lpfem_step + lpfem_get_fields to host)",
+                      "create_ms": 1e3 * t_create, "steps_ms": 1e3 * (el - t_create)}
         sim2.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg)
