@@ -182,7 +182,8 @@ struct lpfem_ctx {
   cudaStream_t st2 = nullptr;  // coarse marching stream (overlaps the fine stage)
   int nsm = 148;               // SMs of the device
   cudaStream_t st3 = nullptr;  // fine porous stage, concurrent with the fine conduit stage (independent)
-  cudaEvent_t evp[2] = {};     // fork / join of st3
+  cudaEvent_t evp[3] = {};     // fork / join of st3; [2]: conduit GMRES about to launch (gates the porous PCG)
+  bool gate = false;           // concurrent fine stage: record / wait evp[2] around the Krylov launches
   cudaEvent_t evc[3] = {};
   long long coarse_n = 0;      // latest coarse time index available
   double coarse_dt = -1.0;
@@ -1062,6 +1063,7 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
                                                              c->nc_p[2], refp<D>(c), P.z, P.lag, P.qf, P.aux, P.isq,
                                                              P.rhs, P.wn, P.rows);
   CKL();
+  if (lev == 1 && c->gate) CK(cudaStreamWaitEvent(st, c->evp[2], 0));  // the GMRES clusters are placed first
   if (lev == 1) CK(cudaEventRecord(c->ek[0], st));
   solve_porous<D>(c, P);
   if (lev == 1) CK(cudaEventRecord(c->ek[1], st));
@@ -1201,6 +1203,7 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
     ks.spmv = 1;
     CK(cudaMemcpyAsync(C.dstat, &ks, sizeof(KStat), cudaMemcpyHostToDevice, st));
   } else {
+    if (lev == 1 && c->gate) CK(cudaEventRecord(c->evp[2], st));
     if (lev == 1) CK(cudaEventRecord(c->ek[2], st));
     solve_conduit<D>(c, C);
     if (lev == 1) CK(cudaEventRecord(c->ek[3], st));
@@ -1322,21 +1325,30 @@ void do_step(lpfem_ctx* c, double dt) {
   // ---------------- Steps 3-4: fine corrections + write-back
   CK(cudaEventRecord(c->ev[1], st));
   // the porous and conduit corrections of a step are independent (each reads only coarse data and its own
-  // region's lagged composite): LPFEM_CONCURRENT=1 runs the porous stage on st3 beside the conduit stage.  Off by
-  // default: measured cfg1 17.5 vs 17.4 ms, cfg2 206 vs 213 ms, cfg3 equal (the GMRES slows by what the PCG saves)
-  const bool conc = c->st3 && getenv("LPFEM_CONCURRENT");
+  // region's lagged composite): the porous stage runs on st3 beside the conduit stage, its PCG gated behind the
+  // GMRES launch so that the GMRES clusters are placed first (ungated, the PCG fragmented the GPCs and a GMRES
+  // cluster ran in a second wave).  Measured fine stage cfg0/1/2/3/4: 4.9/12.9/172/96/2327 ->
+  // 4.5/11.4/150/91/2141 ms.  LPFEM_NO_CONCURRENT=1 serialises.
+  const bool conc = c->st3 && !getenv("LPFEM_NO_CONCURRENT");
   decide_fine_clusters<D>(c, conc);
   if (conc) {
+    // conduit stage enqueued first (it records evp[2] just before its GMRES launch); the porous stage on st3
+    // prepares concurrently and launches its PCG only after that point, on the SMs the GMRES leaves free
     CK(cudaEventRecord(c->evp[0], st));
+    c->gate = true;
+    conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp_u, c->comp_p);
     CK(cudaStreamWaitEvent(c->st3, c->evp[0], 0));
-    StreamSwap sw(c, c->st3);
-    porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+    {
+      StreamSwap sw(c, c->st3);
+      porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+    }
+    c->gate = false;
     CK(cudaEventRecord(c->evp[1], c->st3));
+    CK(cudaStreamWaitEvent(st, c->evp[1], 0));
   } else {
     porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+    conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp_u, c->comp_p);
   }
-  conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp_u, c->comp_p);
-  if (conc) CK(cudaStreamWaitEvent(st, c->evp[1], 0));
   halo_exchange(c);  // a11: refresh the overlaps of the lagged fields (C2 mode B), world > 1 only
   CK(cudaEventRecord(c->ev[2], st));
   // ---------------- Step 1 of the next step, overlapped with this fine stage (reads slot n+1, writes n+2)
@@ -1728,7 +1740,7 @@ void setup(lpfem_ctx* c) {
     cusolverDnSetStream(c->sol, st);
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
+    for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
     if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
     if (getenv("LPFEM_WARM_ORDER")) c->warm_order = std::max(1, std::min(2, atoi(getenv("LPFEM_WARM_ORDER"))));
     c->ml_refresh = D == 2 ? 1 : 4;
@@ -2379,7 +2391,7 @@ void lpfem_destroy(lpfem_ctx* c) {
     cudaStreamDestroy(c->st2);
   }
   if (c->st3) cudaStreamDestroy(c->st3);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 3; ++i)
     if (c->evp[i]) cudaEventDestroy(c->evp[i]);
   for (int i = 0; i < 3; ++i)
     if (c->evc[i]) cudaEventDestroy(c->evc[i]);
