@@ -18,6 +18,7 @@ namespace lp {
 struct ConduitCoefs {
   double eta, nu, alpha, rho, mu, kF, dt;
   double schur_w;  // pressure scaling numerator: nu + h^2/(c dt) (preconditioner only)
+  double vel_w;    // velocity scaling factor of the preconditioner levels (1: plain Jacobi)
 };
 
 template <int D>
@@ -146,7 +147,7 @@ __global__ void k_conduit_scale(const SysDesc* __restrict__ sys, Level L, Condui
   if (r < D * S.n2) {
     unlex<D>(r % S.n2, S.np, l);
     const bool fixed = node_class<D>(L.G, S, l) >= CL_ART;
-    v = fixed ? 0.0 : 1.0 / aconst[find_slot(col, rb, re, r)];
+    v = fixed ? 0.0 : cc.vel_w / aconst[find_slot(col, rb, re, r)];
   } else {
     const int shp1[3] = {S.nc[0] + 1, S.nc[1] + 1, S.nc[2] + 1};
     unlex<D>(r - D * S.n2, shp1, l);

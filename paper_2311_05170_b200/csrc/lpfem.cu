@@ -211,6 +211,7 @@ struct lpfem_ctx {
   long long nstep = 0;
   double cur_dt = -1.0;
   double schur_c = 1.0;
+  double vw = 1.0, pw = 1.0;  // preconditioner scaling weights (velocity levels, pressure Schur approximation)
   // multilevel preconditioner of the fine conduit systems (mlprec.cuh)
   int nl = 0;
   Level Llv[NLMAX];
@@ -733,7 +734,8 @@ ConduitCoefs conduit_coefs(const lpfem_ctx* c, double dt, double hmin) {
   cc.mu = c->co.mu;
   cc.kF = c->co.k[2];
   cc.dt = dt;
-  cc.schur_w = c->co.nu + hmin * hmin / (c->schur_c * dt);
+  cc.schur_w = c->pw * (c->co.nu + hmin * hmin / (c->schur_c * dt));
+  cc.vel_w = c->vw;
   return cc;
 }
 
@@ -1742,6 +1744,9 @@ void setup(lpfem_ctx* c) {
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
     if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
+    if (getenv("LPFEM_VEL_W")) c->vw = atof(getenv("LPFEM_VEL_W"));      // experiment knobs
+    if (getenv("LPFEM_P_W")) c->pw = atof(getenv("LPFEM_P_W"));
+    if (getenv("LPFEM_SCHUR_C")) c->schur_c = atof(getenv("LPFEM_SCHUR_C"));
     if (getenv("LPFEM_WARM_ORDER")) c->warm_order = std::max(1, std::min(2, atoi(getenv("LPFEM_WARM_ORDER"))));
     c->ml_refresh = D == 2 ? 1 : 4;
     if (getenv("LPFEM_ML_REFRESH")) c->ml_refresh = std::max(1, atoi(getenv("LPFEM_ML_REFRESH")));
