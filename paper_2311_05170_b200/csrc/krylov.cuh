@@ -549,16 +549,27 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     // exact coarse-box solve: LZ_L = A_L^-1 LR_L (row-major inverse, warp per row)
     const SysDesc SC = P.lsys[P.nl - 1][bx];
     const int n = SC.nrows;
-    const double* Ai = P.aci + P.aoff[sid];
     const double* rc = LRp(P.nl - 1);
     double* zc = LZp(P.nl - 1);
     const int lane = threadIdx.x & 31;
-    for (int i = gt >> 5; i < n; i += gs >> 5) {
-      double s = 0.0;
+    if (P.acif) {
+      const float* Ai = P.acif + P.aoff[sid];
+      for (int i = gt >> 5; i < n; i += gs >> 5) {
+        double s = 0.0;
 #pragma unroll 4
-      for (int j = lane; j < n; j += 32) s += Ai[(long long)i * n + j] * rc[j];
-      s = warp_sum(s);
-      if (lane == 0) zc[i] = s;
+        for (int j = lane; j < n; j += 32) s += (double)Ai[(long long)i * n + j] * rc[j];
+        s = warp_sum(s);
+        if (lane == 0) zc[i] = s;
+      }
+    } else {
+      const double* Ai = P.aci + P.aoff[sid];
+      for (int i = gt >> 5; i < n; i += gs >> 5) {
+        double s = 0.0;
+#pragma unroll 4
+        for (int j = lane; j < n; j += 32) s += Ai[(long long)i * n + j] * rc[j];
+        s = warp_sum(s);
+        if (lane == 0) zc[i] = s;
+      }
     }
     SUBPHASE(6);
     cl.sync();

@@ -218,7 +218,7 @@ struct lpfem_ctx {
   Family lvl[NLMAX];
   MLArgs ml{};
   double *part = nullptr, *aci = nullptr, *abuf = nullptr, *lwk = nullptr;
-  double* ainv[2] = {nullptr, nullptr};  // row-major coarse-box inverses, double-buffered (coarse_box_inverses)
+  float* ainv[2] = {nullptr, nullptr};   // row-major coarse-box inverses (fp32), double-buffered (coarse_box_inverses)
   int ml_next = 0, ml_busy = 0;          // slot the next fine step uses / slot the enqueued fine step reads
   int warm_order = 2;                    // Krylov initial guess: 1 previous solution, 2 linear extrapolation
   // coarse Navier-Stokes chord iteration: LU of the last factorised Jacobian in `dense`/`piv` (conduit_solve_once)
@@ -1131,7 +1131,7 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
         throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (coarse box)");
     }
   }
-  k_inv_rowmajor<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, cm, c->ainv[slot]);
+  k_inv_rowmajor<float><<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, cm, c->ainv[slot]);
   CKL();
 }
 
@@ -1168,7 +1168,8 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   const bool ml = lev == 1 && c->nl > 0;
   if (ml) {  // coarse-box inverses built by coarse_step (coarse stream, one step ahead)
     c->ml_busy = c->ml_next;
-    c->ml.aci = c->ainv[c->ml_busy];
+    c->ml.acif = c->ainv[c->ml_busy];
+    c->ml.aci = nullptr;
   }
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
@@ -1580,8 +1581,8 @@ void setup(lpfem_ctx* c) {
       c->part = dalloc<double>(ptot);
       c->aci = dalloc<double>(atot);
       c->abuf = dalloc<double>(atot);
-      c->ainv[0] = dalloc<double>(atot);
-      c->ainv[1] = dalloc<double>(atot);
+      c->ainv[0] = dalloc<float>(atot);
+      c->ainv[1] = dalloc<float>(atot);
       c->gjperm = dalloc<int>(atot);
       c->dpoff = dalloc<long long>(poff.size());
       c->daoff = dalloc<long long>(aoff.size());

@@ -25,6 +25,8 @@ struct MLArgs {
   double* LZ[NLMAX];            // level corrections
   const double* LS[NLMAX];      // level scalings (0 on fixed rows)
   const double* aci;            // dense inverses of the coarse-level systems (row-major), at aoff[sid]
+  const float* acif;            // same stored in fp32 (conduit): the preconditioner is then a different but
+                                // fixed linear operator; right-preconditioned GMRES still meets C19 exactly
   const long long* aoff;
   const SysDesc* fsys;          // fine boxes
   const double* s0;             // fine scaling (0 on fixed rows)
@@ -430,18 +432,19 @@ __global__ void __launch_bounds__(NT) k_gj_inverse(const SysDesc* __restrict__ s
 }
 
 // row-major copy of the column-major inverses with the rows and columns of fixed DOFs zeroed
+template <class T>
 __global__ void k_inv_rowmajor(const SysDesc* __restrict__ sys, const double* __restrict__ mask,
                                const long long* __restrict__ aoff, const double* __restrict__ Acm,
-                               double* __restrict__ Arm) {
+                               T* __restrict__ Arm) {
   const SysDesc S = sys[blockIdx.y];
   int i = blockIdx.x;  // row
   if (i >= S.nrows) return;
   const int n = S.nrows;
   const double* src = Acm + aoff[blockIdx.y];
-  double* dst = Arm + aoff[blockIdx.y] + (long long)i * n;
+  T* dst = Arm + aoff[blockIdx.y] + (long long)i * n;
   const bool fi = mask[S.row_off + i] == 0.0;
   for (int j = threadIdx.x; j < n; j += blockDim.x)
-    dst[j] = (fi || mask[S.row_off + j] == 0.0) ? 0.0 : src[(long long)j * n + i];
+    dst[j] = (T)((fi || mask[S.row_off + j] == 0.0) ? 0.0 : src[(long long)j * n + i]);
 }
 
 __global__ void k_set_identity(const SysDesc* __restrict__ sys, const long long* __restrict__ aoff,
