@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--alg1", action="store_true",
+                    help="Algorithm 1 on T_h (the traditional partitioned scheme, P:356-396): the config with H = h")
     return ap.parse_args()
 
 
@@ -180,6 +182,9 @@ def main():
     if world > 1:
         dist.barrier()
     cfg = I.config(args.config)
+    if args.alg1:  # H = h: the coarse step is the fine step, the corrections vanish (DESIGN §8(f) rank 2)
+        cfg = I.config(args.config, H=cfg["h"], overlap=cfg["h"])
+        cfg["name"] += "-alg1"
     D = I.fine_dofs(cfg)
     stream = torch.cuda.Stream()
     nid = None

@@ -1333,8 +1333,17 @@ void do_step(lpfem_ctx* c, double dt) {
   // cluster ran in a second wave).  Measured fine stage cfg0/1/2/3/4: 4.9/12.9/172/96/2327 ->
   // 4.5/11.4/150/91/2141 ms.  LPFEM_NO_CONCURRENT=1 serialises.
   const bool conc = c->st3 && !getenv("LPFEM_NO_CONCURRENT");
-  decide_fine_clusters<D>(c, conc);
-  if (conc) {
+  const bool alg1 = c->R == 1 && !getenv("LPFEM_NO_ALG1_FASTPATH");
+  if (!alg1) decide_fine_clusters<D>(c, conc);
+  if (alg1) {
+    // H = h: the coarse step is Algorithm 1 on T_h and every correction of Steps 3-4 vanishes
+    // identically (the local problems' right-hand sides are the residuals of the converged coarse step in the
+    // same space): the composite is the coarse state n+1 (same mesh, same layout)
+    for (int f = 0; f < 3; ++f)
+      CK(cudaMemcpyAsync(c->comp[f], c->cst[sn][f], c->n2p_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->comp_u, c->cu[sn], (size_t)D * c->n2c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->comp_p, c->cp[sn], c->n1c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else if (conc) {
     // conduit stage enqueued first (it records evp[2] just before its GMRES launch); the porous stage on st3
     // prepares concurrently and launches its PCG only after that point, on the SMs the GMRES leaves free
     CK(cudaEventRecord(c->evp[0], st));
@@ -1362,12 +1371,16 @@ void do_step(lpfem_ctx* c, double dt) {
       c->coarse_n = n + 1;  // recomputed (and reported) at the next step
     }
   }
-  fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
-  fetch_stats(c, c->fam[1][1], 1, false, maxres[1], ok);
+  if (!alg1) {
+    fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
+    fetch_stats(c, c->fam[1][1], 1, false, maxres[1], ok);
+  } else {
+    CK(cudaStreamSynchronize(st));
+  }
   float ms1 = 0, mk0 = 0, mk1 = 0;
   CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
-  if (!c->fam[1][0].hs.empty()) CK(cudaEventElapsedTime(&mk0, c->ek[0], c->ek[1]));
-  if (!c->fam[1][1].hs.empty()) CK(cudaEventElapsedTime(&mk1, c->ek[2], c->ek[3]));
+  if (!alg1 && !c->fam[1][0].hs.empty()) CK(cudaEventElapsedTime(&mk0, c->ek[0], c->ek[1]));
+  if (!alg1 && !c->fam[1][1].hs.empty()) CK(cudaEventElapsedTime(&mk1, c->ek[2], c->ek[3]));
   c->stats.t_krylov_ms[0] += mk0;
   c->stats.t_krylov_ms[1] += mk1;
   c->stats.kernel_launches += tl_launches;
@@ -1516,7 +1529,8 @@ void setup(lpfem_ctx* c) {
         rs.push_back(r);
       }
     }
-    if (aligned && (int)rs.size() <= NLMAX) {
+    // R = 1 (H = h): Algorithm 1 on T_h, no fine corrections are solved (do_step), so no multilevel setup
+    if (aligned && (int)rs.size() <= NLMAX && c->R > 1) {
       c->nl = (int)rs.size();
       std::vector<long long> poff, aoff;
       long long ptot = 0, atot = 0;

@@ -153,3 +153,24 @@ def test_dt_change_reassembles_and_converges():
     f = sim.fields()
     assert all(np.isfinite(np.ravel(v)).all() for v in f.values())
     sim.close()
+
+
+@pytest.mark.parametrize("dim,h,dt", [(2, 1 / 16, 0.1), (3, 1 / 4, 0.1)])
+def test_parity_algorithm1_on_fine_mesh(dim, h, dt):
+    """with H = h the library marches Algorithm 1 on T_h (the traditional
+    partitioned scheme the paper compares against).  Parity against the oracle's own Algorithm 1 (oracle/alg1.py),
+    C20 bar, every step."""
+    from oracle import alg1
+    from oracle import mesh as M
+    from paper_2311_05170_b200 import LPFEM
+    cfg = I.make_config(dim=dim, H=h, h=h, grid=2, dt=dt, steps=3, problem="mms")
+    Gp, Gc = M.region_grids(cfg, "h")
+    ora = alg1.Alg1(cfg, Gp, Gc, 1)
+    sim = LPFEM(cfg)
+    for n in range(cfg["steps"]):
+        ora.step()
+        sim.step()
+        o = {k: np.asarray(v) for k, v in ora.state.items()}
+        errs, bad = compare(sim.fields(), o)
+        assert not bad, f"step {n + 1}: {errs}"
+    sim.close()
