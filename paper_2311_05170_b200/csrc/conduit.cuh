@@ -269,8 +269,16 @@ __global__ void k_conduit_step(const SysDesc* __restrict__ sys, Level L, Conduit
                                double* __restrict__ aout, double* __restrict__ rhs) {
   const SysDesc S = sys[blockIdx.y];
   int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= S.nrows) return;
   constexpr int N = n2_of(D);
+  // the convection tensor in shared memory: every thread reads C3[i] slabs for its own local node i (divergent
+  // across the warp), which from L1 serialised into one wavefront per distinct line
+  constexpr int NC3 = N * N * N * (D + 1);
+  __shared__ double sC3[NC3];
+  if ((int)(blockIdx.x * blockDim.x) >= S.nrows) return;  // block-uniform
+  for (int k = threadIdx.x; k < NC3; k += blockDim.x) sC3[k] = (&ref->C3[0][0][0][0])[k];
+  __syncthreads();
+  if (r >= S.nrows) return;
+  auto C3 = [&](int i, int m, int j, int k) -> double { return sC3[((i * N + m) * N + j) * (D + 1) + k]; };
   const int nHp[3] = {nHp0, nHp1, nHp2};
   const long long o = S.row_off;
   const long long rb = rowptr[o + r], re = rowptr[o + r + 1];
@@ -312,7 +320,7 @@ __global__ void k_conduit_step(const SysDesc* __restrict__ sys, Level L, Conduit
         // convection eta int phi_i (W.grad phi_j)
         double cv = 0.0;
         for (int k = 0; k <= D; ++k)
-          for (int m = 0; m < N; ++m) cv += ref->C3[i][m][j][k] * wl[k][m];
+          for (int m = 0; m < N; ++m) cv += C3(i, m, j, k) * wl[k][m];
         cv *= ev;
         aout[p0 + a * Ln] += cv;
         b += vol * ref->M22[i][j] * (cc.eta * Fs[idx[j]] + (cc.eta / cc.dt) * Ls[idx[j]]);
@@ -323,7 +331,7 @@ __global__ void k_conduit_step(const SysDesc* __restrict__ sys, Level L, Conduit
             double rv = 0.0;
             for (int m = 0; m < N; ++m) {
               double t2 = 0.0;
-              for (int k = 0; k <= D; ++k) t2 += ref->C3[i][j][m][k] * G[k][bb];
+              for (int k = 0; k <= D; ++k) t2 += C3(i, j, m, k) * G[k][bb];
               rv += We[a][m] * t2;
             }
             aout[p0 + bb * Ln] += ev * rv;

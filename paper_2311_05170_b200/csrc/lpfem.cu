@@ -1100,7 +1100,7 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
   double hmin = 1e300;
   for (int a = 0; a < D; ++a) hmin = std::min(hmin, L.G.hc[a]);
   const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
-  k_conduit_step<D><<<grid_rows(F.maxrows, ns), 128, 0, st>>>(F.ds, L, cc, 1, c->kmult, c->nc_p[0], c->nc_p[1],
+  k_conduit_step<D><<<grid_rows(F.maxrows, ns, 256), 256, 0, st>>>(F.ds, L, cc, 1, c->kmult, c->nc_p[0], c->nc_p[1],
                                                                c->nc_p[2], refp<D>(c), F.rowptr, F.col, F.aconst,
                                                                F.mask, F.z, F.W, F.lag, F.qf, F.aux, F.aout, F.rhs);
   CKL();
@@ -1173,7 +1173,7 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   }
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
-  k_conduit_step<D><<<grid_rows(C.maxrows, ns), 128, 0, st>>>(C.ds, c->Lc[lev], cc, newton, c->kmult,
+  k_conduit_step<D><<<grid_rows(C.maxrows, ns, 256), 256, 0, st>>>(C.ds, c->Lc[lev], cc, newton, c->kmult,
                                                                c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), C.rowptr,
                                                                C.col, C.aconst, colscale, C.z, C.W, C.lag, C.qf, C.aux,
                                                                C.aout, C.rhs);
