@@ -258,8 +258,14 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
 
 // Per-step operator: A' = mask * (A_const + eta N(W) [+ eta R(U)]) * diag(s) and right-hand side
 // rhs = mask * (b_load - A z), b_load = eta M f + (eta/dt) M u~^n [+ eta N(U) U] + Gamma loads.
+// 254 registers in 3D (low occupancy) is the measured optimum: forcing 2 or 3 blocks of 256 per SM spills and
+// runs 5% / 24% slower (cfg4 226 -> 236 / 280 ms)
+#ifndef LPFEM_CSTEP_MINB
+#define LPFEM_CSTEP_MINB 1
+#endif
 template <int D>
-__global__ void k_conduit_step(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int newton,
+__global__ void __launch_bounds__(256, LPFEM_CSTEP_MINB)
+k_conduit_step(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int newton,
                                const double* __restrict__ kmult, int nHp0, int nHp1, int nHp2,
                                const RefT<D>* __restrict__ ref, const long long* __restrict__ rowptr,
                                const int* __restrict__ col, const double* __restrict__ aconst,
