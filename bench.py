@@ -71,6 +71,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs ~0.1-0.5 s to start: wait for its first sample so that short timed regions
+            # (cfg0: ~15 ms) are still sampled
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -81,6 +86,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.06)  # one more sample at the end of the timed region
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
