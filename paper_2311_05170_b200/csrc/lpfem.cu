@@ -221,6 +221,13 @@ struct lpfem_ctx {
   float* ainv[2] = {nullptr, nullptr};   // row-major coarse-box inverses (fp32), double-buffered (coarse_box_inverses)
   int ml_next = 0, ml_busy = 0;          // slot the next fine step uses / slot the enqueued fine step reads
   int warm_order = 2;                    // Krylov initial guess: 1 previous solution, 2 linear extrapolation
+  // experiment switches (environment, read once at create)
+  struct Knobs {
+    bool verbose = false, no_smem_pattern = false, cold_start = false, coarse_full_newton = false;
+    bool no_concurrent = false, no_alg1_fastpath = false, no_overlap = false;
+    double reorth2 = 0.1;
+    int gj_max = 512;
+  } kn;
   // coarse Navier-Stokes chord iteration: LU of the last factorised Jacobian in `dense`/`piv` (conduit_solve_once)
   bool clu_valid = false, clu_force = false;
   int clu_newton = -1;
@@ -654,7 +661,7 @@ void launch_cluster_sm(Kern k, int nsys, int CL, int NT, size_t smem, cudaStream
 // Returns the largest cluster size <= CLmax whose clusters all fit (any size, not only powers of two: the GPCs
 // of a B200 are not all the same size), by the occupancy API.
 template <class Kern>
-int resident_cluster(Kern k, int nsys, int CLmax, int NT, size_t smem) {
+int resident_cluster(Kern k, int nsys, int CLmax, int NT, size_t smem, bool verbose = false) {
   for (int CL = CLmax; CL > 1; --CL) {
     if (CL > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     if (smem > 0) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -674,7 +681,7 @@ int resident_cluster(Kern k, int nsys, int CLmax, int NT, size_t smem) {
       cudaGetLastError();
       continue;
     }
-    if (getenv("LPFEM_VERBOSE")) fprintf(stderr, "[lpfem] cluster %d: %d systems, %d resident clusters\n", CL, nsys, ncl);
+    if (verbose) fprintf(stderr, "[lpfem] cluster %d: %d systems, %d resident clusters\n", CL, nsys, ncl);
     if (ncl >= nsys) return CL;
   }
   return 1;
@@ -689,8 +696,8 @@ void launch_cluster(Kern k, int nsys, int CL, int NT, cudaStream_t st, const Arg
 // largest (row offsets + column indices) of any CTA's row block, or 0 when one does not fit next to the
 // kernel's static shared memory (the kernels then read the pattern from global memory).
 template <class Kern>
-size_t pattern_smem(Kern k, const Family& F, int CL, size_t front = 0) {
-  if (getenv("LPFEM_NO_SMEM_PATTERN") || F.hrp.empty()) return 0;
+size_t pattern_smem(Kern k, const Family& F, int CL, size_t front = 0, bool disabled = false) {
+  if (disabled || F.hrp.empty()) return 0;
   cudaFuncAttributes at;
   CK(cudaFuncGetAttributes(&at, k));
   const long long budget = 227LL * 1024 - (long long)at.sharedSizeBytes - (long long)front - 1024;
@@ -850,7 +857,7 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.maxit = c->opts.max_iter;
   a.stat = P.dstat;
   // warm start from the previous step's corrections (fine ML-PCG): measured fewer iterations, same test (C19)
-  a.warm = (P.level == 1 && c->nlp > 0 && !getenv("LPFEM_COLD_START")) ? std::min(P.solved, c->warm_order) : 0;
+  a.warm = (P.level == 1 && c->nlp > 0 && !c->kn.cold_start) ? std::min(P.solved, c->warm_order) : 0;
   if (a.warm > 0 && !P.xp) {
     P.xp = dalloc<double>(3 * P.rows);
     CK(cudaMemsetAsync(P.xp, 0, 3 * P.rows * sizeof(double), c->st));
@@ -860,19 +867,19 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   const int ns = (int)P.hk.size();
   auto go_ml = [&](auto k) {
     if (!P.cluster_checked && !P.bandwidth_bound) {
-      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster));
+      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern), c->kn.verbose);
       P.cluster_checked = true;
     }
-    const size_t sm = pattern_smem(k, P, P.cluster);
+    const size_t sm = pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern);
     a.smem_cols = sm > 0;
     launch_cluster_sm(k, ns, P.cluster, 1024, sm, c->st, a, c->mlp, P.zv);
   };
   auto go = [&](auto k) {
     if (!P.cluster_checked && !P.bandwidth_bound) {
-      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster));
+      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern), c->kn.verbose);
       P.cluster_checked = true;
     }
-    const size_t sm = pattern_smem(k, P, P.cluster);
+    const size_t sm = pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern);
     a.smem_cols = sm > 0;
     launch_cluster_sm(k, ns, P.cluster, 1024, sm, c->st, a);
   };
@@ -905,7 +912,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
-  a.warm = (C.level == 1 && !getenv("LPFEM_COLD_START")) ? std::min(C.solved, c->warm_order) : 0;
+  a.warm = (C.level == 1 && !c->kn.cold_start) ? std::min(C.solved, c->warm_order) : 0;
   if (a.warm > 0 && !C.xp) {
     C.xp = dalloc<double>(C.rows);
     CK(cudaMemsetAsync(C.xp, 0, C.rows * sizeof(double), c->st));
@@ -914,7 +921,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   C.solved = std::min(C.solved + 1, 2);
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
   // threshold reorthogonalised almost every iteration for identical iteration counts (cfg1-3), +20% GMRES time
-  a.reorth2 = getenv("LPFEM_REORTH2") ? atof(getenv("LPFEM_REORTH2")) : 0.1;
+  a.reorth2 = c->kn.reorth2;
 #ifdef LPFEM_PHASE_TIMERS
   static long long* ph = nullptr;
   const int nsys_ph = (int)C.hk.size();
@@ -928,10 +935,10 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   const size_t hb = gmres_h_bytes(GM);
   auto go = [&](auto k) {
     if (!C.cluster_checked && !C.bandwidth_bound) {
-      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb));
+      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern), c->kn.verbose);
       C.cluster_checked = true;
     }
-    const size_t sm = pattern_smem(k, C, C.cluster, hb);
+    const size_t sm = pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern);
     a.smem_cols = sm > 0;
     launch_cluster_sm(k, (int)C.hk.size(), C.cluster, NTG, hb + sm, c->st, a, c->ml);
   };
@@ -982,7 +989,7 @@ void decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
   if (!C.hk.empty() && !C.cluster_checked && !C.bandwidth_bound) {
     const size_t hb = gmres_h_bytes(GM);
     auto chk = [&](auto k) {
-      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb));
+      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern), c->kn.verbose);
       C.cluster_checked = true;
     };
     const bool pc = c->nl > 0;
@@ -1111,7 +1118,7 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
   int nmax = 1;
   for (auto& S2 : F.hs) nmax = std::max(nmax, S2.nrows);
   const double* cm = c->aci;  // column-major inverses
-  if (nmax <= (getenv("LPFEM_GJ_MAX") ? atoi(getenv("LPFEM_GJ_MAX")) : 512)) {
+  if (nmax <= c->kn.gj_max) {
     // small boxes (2D): batched in-place Gauss-Jordan, one CTA per matrix
     const size_t smem = 2 * (size_t)nmax * sizeof(double);
     k_gj_inverse<1024><<<ns, 1024, smem, st>>>(F.ds, c->daoff, c->abuf, c->gjperm);
@@ -1264,7 +1271,7 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
     if (!(du == du)) break;  // NaN: diverged
     // chord iteration: refactorise at the current iterate when the frozen Jacobian contracts too slowly
     // (or diverges); LPFEM_COARSE_FULL_NEWTON refactorises every iteration (plain Newton / Picard)
-    if (getenv("LPFEM_COARSE_FULL_NEWTON") || (it > 0 && du > 0.25 * du_prev) || it >= 12) c->clu_force = true;
+    if (c->kn.coarse_full_newton || (it > 0 && du > 0.25 * du_prev) || it >= 12) c->clu_force = true;
     du_prev = du;
     if (du <= c->opts.picard_rtol * un || du <= 1e-14 * std::sqrt((double)nu)) {
       pic_ok = true;
@@ -1332,8 +1339,8 @@ void do_step(lpfem_ctx* c, double dt) {
   // GMRES launch so that the GMRES clusters are placed first (ungated, the PCG fragmented the GPCs and a GMRES
   // cluster ran in a second wave).  Measured fine stage cfg0/1/2/3/4: 4.9/12.9/172/96/2327 ->
   // 4.5/11.4/150/91/2141 ms.  LPFEM_NO_CONCURRENT=1 serialises.
-  const bool conc = c->st3 && !getenv("LPFEM_NO_CONCURRENT");
-  const bool alg1 = c->R == 1 && !getenv("LPFEM_NO_ALG1_FASTPATH");
+  const bool conc = c->st3 && !c->kn.no_concurrent;
+  const bool alg1 = c->R == 1 && !c->kn.no_alg1_fastpath;
   if (!alg1) decide_fine_clusters<D>(c, conc);
   if (alg1) {
     // H = h: the coarse step is Algorithm 1 on T_h and every correction of Steps 3-4 vanishes
@@ -1364,7 +1371,7 @@ void do_step(lpfem_ctx* c, double dt) {
   halo_exchange(c);  // a11: refresh the overlaps of the lagged fields (C2 mode B), world > 1 only
   CK(cudaEventRecord(c->ev[2], st));
   // ---------------- Step 1 of the next step, overlapped with this fine stage (reads slot n+1, writes n+2)
-  if (c->overlap && !getenv("LPFEM_NO_OVERLAP")) {
+  if (c->overlap && !c->kn.no_overlap) {
     try {
       coarse_step<D>(c, n + 1, dt);
     } catch (const Err&) {
@@ -1758,6 +1765,18 @@ void setup(lpfem_ctx* c) {
     CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
+    {
+      auto on = [](const char* k) { return getenv(k) != nullptr; };
+      c->kn.verbose = on("LPFEM_VERBOSE");
+      c->kn.no_smem_pattern = on("LPFEM_NO_SMEM_PATTERN");
+      c->kn.cold_start = on("LPFEM_COLD_START");
+      c->kn.coarse_full_newton = on("LPFEM_COARSE_FULL_NEWTON");
+      c->kn.no_concurrent = on("LPFEM_NO_CONCURRENT");
+      c->kn.no_alg1_fastpath = on("LPFEM_NO_ALG1_FASTPATH");
+      c->kn.no_overlap = on("LPFEM_NO_OVERLAP");
+      if (on("LPFEM_REORTH2")) c->kn.reorth2 = atof(getenv("LPFEM_REORTH2"));
+      if (on("LPFEM_GJ_MAX")) c->kn.gj_max = atoi(getenv("LPFEM_GJ_MAX"));
+    }
     if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
     if (getenv("LPFEM_VEL_W")) c->vw = atof(getenv("LPFEM_VEL_W"));      // experiment knobs
     if (getenv("LPFEM_P_W")) c->pw = atof(getenv("LPFEM_P_W"));
