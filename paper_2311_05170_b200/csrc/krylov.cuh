@@ -517,7 +517,32 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
   auto LRp = [&](int l) { return P.LR[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
   auto LZp = [&](int l) { return P.LZ[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
   auto LSp = [&](int l) { return P.LS[l] + f * P.lstride[l] + P.lsys[l][bx].row_off; };
-  if (P.direct) {
+  if (P.direct == 2) {
+    // level 0 from the fine vector, then every coarser level directly from level 0 in one phase; coarse solve;
+    // z_0 = S_0 r_0 + sum_{0<l<L} P_{0<-l} S_l r_l + P_{0<-L} z_L in one phase; fine combine.  Four cluster
+    // barriers per application for any number of levels (the sequential chain needs 2 L + 2).
+    {
+      const SysDesc SC = P.lsys[0][bx];
+      double* dst = LRp(0);
+      const int wfirst = (gt & ~31) / RLN;
+      for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN)
+        restrict_item<D, NC, RLN>(S0, SC, P.st[0], v, dst, it, gt % RLN);
+    }
+    cl.sync();
+    if (P.nl > 1) {
+      const SysDesc SL0 = P.lsys[0][bx];
+      int tot = 0;
+      for (int l = 1; l < P.nl; ++l) tot += P.lsys[l][bx].nrows;
+      const int wfirst = (gt & ~31) / RLN;
+      for (int it = gt / RLN, w0 = wfirst; w0 < tot; it += gs / RLN, w0 += gs / RLN) {
+        int l = 1, rem = it < tot ? it : tot - 1;
+        while (rem >= P.lsys[l][bx].nrows) rem -= P.lsys[l++][bx].nrows;
+        const SysDesc SC = P.lsys[l][bx];
+        restrict_item<D, NC, RLN>(SL0, SC, P.st0[l], LRp(0), LRp(l), it < tot ? rem : SC.nrows, gt % RLN);
+      }
+      cl.sync();
+    }
+  } else if (P.direct) {
     // every level restricts the fine vector directly (one phase), coarse solve, one fused fine gather
     int tot = 0;
     for (int l = 0; l < P.nl; ++l) tot += P.lsys[l][bx].nrows;
@@ -573,7 +598,20 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     }
     SUBPHASE(6);
     cl.sync();
-    if (!P.direct) {
+    if (P.direct == 2 && P.nl > 1) {
+      const SysDesc SL0 = P.lsys[0][bx];
+      const double* r0v = LRp(0);
+      const double* s0v = LSp(0);
+      double* z0 = LZp(0);
+      for (int i = gt; i < SL0.nrows; i += gs) {
+        double zi = s0v[i] * r0v[i];
+        for (int l = 1; l < P.nl - 1; ++l)
+          zi += prolong_row<D, NC>(SL0, P.lsys[l][bx], P.q0[l], LRp(l), i, LSp(l));
+        zi += prolong_row<D, NC>(SL0, P.lsys[P.nl - 1][bx], P.q0[P.nl - 1], LZp(P.nl - 1), i);
+        z0[i] = zi;
+      }
+      cl.sync();
+    } else if (!P.direct) {
       for (int l = P.nl - 2; l >= 0; --l) {
         const SysDesc SL = P.lsys[l][bx];
         const SysDesc SU = P.lsys[l + 1][bx];
@@ -594,7 +632,7 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     if (si != 0.0) {
       zi = si * v[i];
       if (P.nl > 0) {
-        if (P.direct) {
+        if (P.direct == 1) {
           for (int l = 0; l < P.nl - 1; ++l)
             zi += prolong_row<D, NC>(S0, P.lsys[l][bx], P.r[l], LRp(l), i, LSp(l));
           zi += prolong_row<D, NC>(S0, P.lsys[P.nl - 1][bx], P.r[P.nl - 1], LZp(P.nl - 1), i);

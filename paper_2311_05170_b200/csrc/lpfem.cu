@@ -1575,10 +1575,21 @@ void setup(lpfem_ctx* c) {
         alloc_vectors(c, F, true);
         c->ml.q[l] = l == 0 ? r : r / rs[l - 1];
         c->ml.r[l] = r;
-        c->ml.direct = getenv("LPFEM_ML_DIRECT") ? 1 : 0;  // experiment: one-phase restriction to all levels
+        c->ml.direct = getenv("LPFEM_ML_DIRECT") ? atoi(getenv("LPFEM_ML_DIRECT")) : 0;  // 1, 2: see MLArgs
+        c->ml.q0[l] = r / rs[0];
+        c->ml.st0[l] = nullptr;
+        if (c->ml.direct == 2 && l > 0) {
+          Stencil* hs0 = new Stencil();
+          build_stencil<D>(r / rs[0], *hs0);
+          Stencil* ds0 = dalloc<Stencil>(1);
+          CK(cudaMemcpy(ds0, hs0, sizeof(Stencil), cudaMemcpyHostToDevice));
+          delete hs0;
+          c->stencils.push_back(ds0);
+          c->ml.st0[l] = ds0;
+        }
         {
           Stencil* hst = new Stencil();
-          build_stencil<D>(c->ml.direct ? r : c->ml.q[l], *hst);
+          build_stencil<D>(c->ml.direct == 1 ? r : c->ml.q[l], *hst);
           Stencil* dst = dalloc<Stencil>(1);
           CK(cudaMemcpy(dst, hst, sizeof(Stencil), cudaMemcpyHostToDevice));
           delete hst;
@@ -1660,6 +1671,8 @@ void setup(lpfem_ctx* c) {
           alloc_vectors(c, F, true);
           F.dinv = dalloc<double>(3 * F.rows);
           c->mlp.q[l] = c->ml.q[l];
+          c->mlp.q0[l] = c->ml.q0[l];
+          c->mlp.st0[l] = c->ml.st0[l];
           c->mlp.r[l] = r;
           c->mlp.st[l] = c->ml.st[l];
           c->mlp.lsys[l] = F.ds;
@@ -1684,7 +1697,7 @@ void setup(lpfem_ctx* c) {
         FP.dinv = dalloc<double>(3 * FP.rows);
         FP.zv = dalloc<double>(3 * FP.rows);
         c->mlp.nl = c->nlp;
-        c->mlp.direct = 0;
+        c->mlp.direct = c->ml.direct == 2 ? 2 : 0;
         c->mlp.nsub = (int)FP.hs.size();
         c->mlp.aci = c->abuf_p;  // row-major inverses
         c->mlp.aoff = c->daoff_p;

@@ -31,7 +31,10 @@ struct MLArgs {
   const SysDesc* fsys;          // fine boxes
   const double* s0;             // fine scaling (0 on fixed rows)
   const struct Stencil* st[NLMAX];  // restriction stencils per level (ratio q[l]; direct mode: ratio r[l])
-  int direct;                   // 1: every level restricts from / prolongs to the fine system directly
+  int direct;                   // 1: every level restricts from / prolongs to the fine system directly;
+                                // 2: level 0 from the fine system, levels 1.. directly from / to level 0
+  const struct Stencil* st0[NLMAX];  // direct == 2: restriction stencils level 0 -> level l (ratio q0[l])
+  int q0[NLMAX];                // direct == 2: ratio of level l to level 0
   int r[NLMAX];                 // ratio of level l to the fine mesh
   int nsub;                     // boxes per field: system sid = field * nsub + box
   long long lstride[NLMAX];     // field stride of the level vectors / scalings
