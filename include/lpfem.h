@@ -82,7 +82,8 @@ typedef struct {
   int lag_mode;         /* LPFEM_LAG_* */
   double krylov_rtol;   /* ||b - A x||_2 <= rtol ||b||_2 on every correction system (C19): 1e-12 */
   int max_iter;         /* per solve, counted in Krylov iterations: e.g. 20000 */
-  int gmres_restart;    /* m of GMRES(m): 30 */
+  int gmres_restart;    /* m of GMRES(m): 0 = the compiled length (45, measured best; LPFEM_GM at build
+                           time); any other value than 0 or that length is LPFEM_EINVAL */
   double picard_rtol;   /* coarse NS: ||du||_2 <= rtol ||u||_2 (C11): 1e-13 */
   int picard_max;       /* 50 */
 } lpfem_opts;
@@ -118,14 +119,20 @@ lpfem_status lpfem_nccl_unique_id(unsigned char out[128]);
 /* Build meshes, subdomains (Algorithm 3 Step 2), patterns and the constant
  * operators; interpolate the initial state (C12).  H, h, overlap are lengths; 1/h, 1/H, H/h and
  * overlap/h must be integers and subdomain_grid[a] must divide the fine cells per axis of each
- * region (the grid applies per region, C8).  Collective. */
+ * region (the grid applies per region, C8).  H == h selects Algorithm 1 on T_h: the coarse
+ * step is then the fine step and every correction vanishes, so lpfem_step marches Algorithm 1 alone
+ * (dense direct solves of the conduit system: meshes up to ~4e4 conduit DOFs).  Collective. */
 lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs, const lpfem_data* data,
                           double H, double h, double overlap, const int subdomain_grid[3],
                           const lpfem_opts* opts, const lpfem_dist* dist, lpfem_ctx** out);
 
 /* One step t_n -> t_{n+1} = (n+1) dt (C18): coarse step, fine corrections on
  * every local subdomain, write-back and halo exchange.  A change
- * of dt re-assembles the porous operators.  On LPFEM_ENOCONV the state stays at t_n.  Collective. */
+ * of dt re-assembles the porous operators.  On LPFEM_ENOCONV the state stays at t_n.  Collective.
+ * The coarse step for t_{n+2} is computed on a side stream while this call's fine stage runs (it is
+ * waited for at the next call); the fine Krylov solves start from the previous steps' corrections
+ * (same stopping test, C19); the coarse Navier-Stokes solve is a chord iteration on the last factorised
+ * Jacobian (same C11 test).  None of these changes the discrete solution beyond the stated tolerances. */
 lpfem_status lpfem_step(lpfem_ctx* ctx, double dt);
 
 /* Node counts of the global fine fields: [porous, conduit]. */

@@ -136,7 +136,7 @@ class LPFEM:
         dat = Data(problem=PROB[cfg["problem"]], inflow_peak=cfg.get("inflow_peak", 1.0),
                    const_value=cfg.get("const_value", 1.0))
         o = Opts(lag_mode=LAG[cfg.get("lag_mode", "composite")], krylov_rtol=cfg.get("krylov_rtol", 1e-12),
-                 max_iter=max_iter, gmres_restart=30, picard_rtol=cfg.get("picard_rtol", 1e-13),
+                 max_iter=max_iter, gmres_restart=0, picard_rtol=cfg.get("picard_rtol", 1e-13),
                  picard_max=cfg.get("picard_max", 50))
         ds = Dist(rank=rank, world=world, device=device, cuda_stream=stream)
         if nccl_id is not None:

@@ -2115,6 +2115,10 @@ lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs
     if (c->opts.max_iter <= 0) c->opts.max_iter = 20000;
     if (c->opts.picard_rtol <= 0) c->opts.picard_rtol = 1e-13;
     if (c->opts.picard_max <= 0) c->opts.picard_max = 50;
+    if (c->opts.gmres_restart != 0 && c->opts.gmres_restart != GM)
+      throw Err(LPFEM_EINVAL, "gmres_restart: 0 (default) or the compiled restart length " + std::to_string(GM) +
+                                  " (LPFEM_GM at build time)");
+    c->opts.gmres_restart = GM;
     if (dist) {
       c->dist = *dist;
     } else {
