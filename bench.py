@@ -273,20 +273,6 @@ def main():
                            "coarse_picard": (st1["picard_iters"] - st0["picard_iters"]) / args.steps},
         "fine_value": D * args.steps / ((st1["t_fine_ms"] - st0["t_fine_ms"]) * 1e-3),
     }
-    # SpMV building block of the Krylov kernels (BASELINE metric "SpMV % HBM peak"): the conduit family's batched
-    # y = A x with the same device routine, L2 flushed before every rep, outside the timed region (measured on
-    # the bench context before it closes; the e2e run below creates its own context)
-    try:
-        sp = sim.bench_spmv(1, reps=10, flush=True)
-        out["spmv"] = {"family": "conduit (fine Oseen operators, all systems of rank 0)", "bound": "hbm",
-                       "achieved": sp["gbs"], "peak": peak, "unit": "GB/s", "frac": sp["gbs"] / peak,
-                       "ms_per_rep": sp["ms"], "algorithmic_bytes_per_rep": sp["bytes"],
-                       "l2": "flushed before every rep"}
-    except Exception as e:  # a rank without conduit systems (small configs on many GPUs)
-        out["spmv"] = {"unavailable": str(e)[:120]}
-    sim.close()
-    del flush
-    torch.cuda.empty_cache()
     # end to end through the public API with host buffers: create from host inputs, K steps, fields -> host
     if not args.no_e2e:
         torch.cuda.synchronize()
@@ -313,6 +299,18 @@ def main():
                       "includes": "lpfem_create (setup, assembly) + K x (lpfem_step + lpfem_get_fields to host)",
                       "create_ms": 1e3 * t_create, "steps_ms": 1e3 * (el - t_create)}
         sim2.close()
+    # SpMV building block of the Krylov kernels (BASELINE metric "SpMV % HBM peak"): the conduit family's batched
+    # y = A x with the same device routine, L2 flushed before every rep, outside the timed region (measured on
+    # the bench context before it closes)
+    try:
+        sp = sim.bench_spmv(1, reps=10, flush=True)
+        out["spmv"] = {"family": "conduit (fine Oseen operators, all systems of rank 0)", "bound": "hbm",
+                       "achieved": sp["gbs"], "peak": peak, "unit": "GB/s", "frac": sp["gbs"] / peak,
+                       "ms_per_rep": sp["ms"], "algorithmic_bytes_per_rep": sp["bytes"],
+                       "l2": "flushed before every rep"}
+    except Exception as e:  # a rank without conduit systems (small configs on many GPUs)
+        out["spmv"] = {"unavailable": str(e)[:120]}
+    sim.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
