@@ -246,6 +246,8 @@ struct lpfem_ctx {
   Level Lplv[NLMAX];
   MLArgs mlp{};
   double *aci_p = nullptr, *abuf_p = nullptr;
+  int* gjperm_p = nullptr;        // porous: pivot scratch of the batched Gauss-Jordan inversion
+  SysDesc* pds3 = nullptr;        // porous coarse-box descriptors, one per (field, box) system
   long long* daoff_p = nullptr;
   std::vector<long long> haoff_p;
   // multi-GPU (world > 1): NCCL communicator, halo plan, exchange buffers
@@ -793,6 +795,21 @@ void porous_levels(lpfem_ctx* c, double dt) {
   k_dense_porous<<<dim3((F.maxrows + 127) / 128, 3 * ns), 128, 0, st>>>(F.ds, ns, F.rowptr, F.col, F.val, F.nnz, F.wn,
                                                                       F.rows, c->daoff_p, c->abuf_p);
   CKL();
+  int nmax = 1;
+  for (auto& S2 : F.hs) nmax = std::max(nmax, S2.nrows);
+  if (nmax <= c->kn.gj_max) {
+    // one batched in-place Gauss-Jordan launch for all (field, box) systems instead of 2 x 3 x boxes cuSOLVER
+    // calls; the column-major inverse in abuf_p, its masked row-major copy in aci_p
+    k_gj_inverse<1024><<<3 * ns, 1024, 2 * (size_t)nmax * sizeof(double), st>>>(c->pds3, c->daoff_p, c->abuf_p,
+                                                                                c->gjperm_p);
+    CKL();
+    k_inv_rowmajor_porous<<<dim3(F.maxrows, 3 * ns), 128, 0, st>>>(F.ds, ns, F.wn, F.rows, c->daoff_p, c->abuf_p,
+                                                                   c->aci_p);
+    CKL();
+    c->mlp.aci = c->aci_p;
+    return;
+  }
+  c->mlp.aci = c->abuf_p;
   k_set_identity_n<<<dim3(F.maxrows, 3 * ns), 128, 0, st>>>(F.ds, ns, c->daoff_p, c->aci_p);
   CKL();
   for (int sid = 0; sid < 3 * ns; ++sid) {
@@ -1692,6 +1709,14 @@ void setup(lpfem_ctx* c) {
         c->haoff_p = aoffp;
         c->aci_p = dalloc<double>(atp);
         c->abuf_p = dalloc<double>(atp);
+        c->gjperm_p = dalloc<int>(atp);
+        {
+          std::vector<SysDesc> h3;
+          for (int f = 0; f < 3; ++f)
+            for (auto& S3 : FL.hs) h3.push_back(S3);
+          c->pds3 = dalloc<SysDesc>(h3.size());
+          CK(cudaMemcpy(c->pds3, h3.data(), h3.size() * sizeof(SysDesc), cudaMemcpyHostToDevice));
+        }
         c->daoff_p = dalloc<long long>(aoffp.size());
         CK(cudaMemcpy(c->daoff_p, aoffp.data(), aoffp.size() * sizeof(long long), cudaMemcpyHostToDevice));
         FP.dinv = dalloc<double>(3 * FP.rows);
@@ -2435,7 +2460,7 @@ void lpfem_destroy(lpfem_ctx* c) {
   if (c->st2) cudaStreamSynchronize(c->st2);
   if (c->st3) cudaStreamSynchronize(c->st3);
   {
-    void* mp[] = {c->gjperm, c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo,
+    void* mp[] = {c->gjperm, c->gjperm_p, c->pds3, c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo,
                   c->ainv[0], c->ainv[1], c->lwk2, c->lpiv2, c->linfo2};
     for (void* p : mp)
       if (p) cudaFree(p);
