@@ -408,6 +408,10 @@ void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
   F.r = dalloc<double>(nv);
   F.p = dalloc<double>(nv);
   CK(cudaMemsetAsync(F.x, 0, nv * sizeof(double), c->st));
+  if (!level_family && F.level == 1) {  // Krylov warm start: the solution one step before x
+    F.xp = dalloc<double>(nv);
+    CK(cudaMemsetAsync(F.xp, 0, nv * sizeof(double), c->st));
+  }
   if (F.kind == 0) {
     F.val = dalloc<double>(3 * F.nnz);
     F.diag = dalloc<double>(nv);
@@ -875,10 +879,6 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.stat = P.dstat;
   // warm start from the previous step's corrections (fine ML-PCG): measured fewer iterations, same test (C19)
   a.warm = (P.level == 1 && c->nlp > 0 && !c->kn.cold_start) ? std::min(P.solved, c->warm_order) : 0;
-  if (a.warm > 0 && !P.xp) {
-    P.xp = dalloc<double>(3 * P.rows);
-    CK(cudaMemsetAsync(P.xp, 0, 3 * P.rows * sizeof(double), c->st));
-  }
   a.xp = a.warm > 0 ? P.xp : nullptr;
   P.solved = std::min(P.solved + 1, 2);
   const int ns = (int)P.hk.size();
@@ -930,10 +930,6 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.stat = C.dstat;
   a.q = C.q;
   a.warm = (C.level == 1 && !c->kn.cold_start) ? std::min(C.solved, c->warm_order) : 0;
-  if (a.warm > 0 && !C.xp) {
-    C.xp = dalloc<double>(C.rows);
-    CK(cudaMemsetAsync(C.xp, 0, C.rows * sizeof(double), c->st));
-  }
   a.xp = a.warm > 0 ? C.xp : nullptr;
   C.solved = std::min(C.solved + 1, 2);
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
