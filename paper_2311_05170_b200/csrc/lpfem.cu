@@ -1746,7 +1746,8 @@ void setup(lpfem_ctx* c) {
         // wave 145 ms; latency-bound families (cfg1) need one wave: cluster 6 14.6 ms vs 8 in 2 waves 20 ms
         long long nzmax = 0;
         for (long long z : F.sys_nnz) nzmax = std::max(nzmax, z);
-        F.bandwidth_bound = nzmax > 2000000;
+        const long long bw_nnz = getenv("LPFEM_BW_NNZ") ? atoll(getenv("LPFEM_BW_NNZ")) : 2000000;  // experiment
+        F.bandwidth_bound = nzmax > bw_nnz;
         if (F.bandwidth_bound) {  // up to two waves: cfg4 cluster 2 / 4 / 8 -> GMRES 1865 / 1777 / 1833 ms
           cl = 1;
           while (cl < 16 && nsys * cl <= nsm) cl *= 2;
