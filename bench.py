@@ -1,32 +1,42 @@
 """Benchmark: fine DOF.steps/s of the local-parallel two-grid FEM hot path (Algorithm 3, arXiv 2311.05170).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
 One "step" = one backward-Euler step of Algorithm 3 through lpfem_step: the coarse step,
 every fine subdomain correction (3 porous PCG solves + 1 conduit GMRES solve per subdomain,
-with assembly, prolongation, RHS) and the write-back.  Workload: BASELINE.json configs[1]
-(2D, H=1/8, h=1/64, 4x4 subdomains, dt=0.05) unless --config says otherwise.  Inputs are synthetic
-(the paper's manufactured solution, seeded), resident in HBM when the timed region starts.
+with assembly, prolongation, RHS) and the write-back.  Workload: BASELINE.json configs[4]
+(3D, H=1/8, h=1/48, 4x4x4 subdomains, injection with log-normal permeability, dt=0.01: 5.59M fine DOFs,
+the largest configuration, in the HBM regime at every GPU count) unless --config says
+otherwise.  Inputs are synthetic (seeded), resident in HBM when the timed region starts.
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events on the library's stream;
-the L2 is flushed (a 512 MiB write) before every timed step because the cfg1 working set fits in L2.
+the L2 is flushed (a 512 MiB write) before every timed step (cfg0/cfg1 fit in L2).
 value = D * K / sum(step times) with D the fine DOF count (3(2N+1)^d + d(2N+1)^d + (N+1)^d).
-Multi-GPU: launched by torchrun; ranks own disjoint subdomain positions (weak scaling of the per-GPU
-work is not applicable: the problem is fixed, scaling is "strong"); max over ranks.
+Multi-GPU: launched by torchrun; ranks own disjoint subdomain positions (LPT placement); the problem is fixed
+as N grows ("strong"); max over ranks.
 
---impl reference: the CPU oracle (oracle/, SciPy SuperLU per subdomain) timed on this host's cores on a
-bounded sample (its first steps of the same workload).
+--impl reference / cpu_baseline: the CPU oracle (oracle/, SciPy SuperLU per subdomain) as it stands, timed on
+this host's cores: one worker process per core, each running the oracle's Algorithm 3 on a share of the subdomain
+positions (its own redundant coarse step, like a GPU rank) with the composite exchanged through the parent every
+step.  cfg0-cfg2 at full size; cfg3 and cfg4 (a single cfg4 conduit factorisation takes 10-30 minutes, SURVEY
+A3) on the same configuration at a coarser fine mesh (h = 1/8 and 1/16, same H, grid, data and coefficients),
+which bounds the oracle's full-size throughput from above (SuperLU cost per DOF grows with the box size).
 """
 from __future__ import annotations
 
-import argparse
-import json
 import os
-import statistics
-import subprocess
-import sys
-import threading
-import time
+
+# the oracle's worker processes run one BLAS thread each: set before numpy (and its BLAS pool) is loaded
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -41,7 +51,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -113,22 +123,146 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def cpu_baseline(cfg: dict, budget_s: float = 20.0) -> dict:
-    """The oracle as it stands (SciPy SuperLU per subdomain), timed on this host: construction excluded,
-    whole steps until ~budget_s of CPU work."""
+# ------------------------------------------------------------------------------------------ CPU oracle legs
+ORACLE_SAMPLE_H = {3: 1 / 8, 4: 1 / 16}  # configs whose full-size oracle step takes hours
+
+
+def oracle_sample_cfg(cfgi: int) -> tuple[dict, str]:
+    cfg = I.config(cfgi)
+    if cfgi in ORACLE_SAMPLE_H:
+        h = ORACLE_SAMPLE_H[cfgi]
+        cfg = I.config(cfgi, h=h)
+        return cfg, (f"cfg{cfgi} structure at h = 1/{round(1 / h)} (same H, grid, data, coefficients, dt; "
+                     f"{I.fine_dofs(cfg)} fine DOFs): an upper bound of the oracle's full-size throughput")
+    return cfg, f"cfg{cfgi} at full size"
+
+
+def _oracle_worker(conn, cfg, positions):
     from oracle import alg3
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    a = alg3.Alg3(cfg)
-    D = I.fine_dofs(cfg)
-    n = 0
-    t0 = time.perf_counter()
-    while n < cfg["steps"] and (n == 0 or time.perf_counter() - t0 < budget_s):
+    from oracle import mesh as M
+    a = alg3.Alg3(cfg, positions=positions)
+    d = cfg["dim"]
+    conn.send("ready")
+    while True:
+        comp = conn.recv()
+        if comp is None:
+            break
+        a.comp = comp
+        f0 = a.timing["fine"]
         a.step()
-        n += 1
-    el = time.perf_counter() - t0
-    return {"value": D * n / el, "unit": "fine DOF*steps/s", "cores": 1, "kind": "oracle",
-            "sample": f"{cfg['name']}: first {n} of {cfg['steps']} steps ({el:.1f} s), construction excluded, "
-                      f"single process (SciPy SuperLU, OPENBLAS_NUM_THREADS=1)"}
+        el = a.timing["fine"] - f0  # the fine stage (Steps 3-4) of this worker's subdomains
+        out = []
+        for P in a.P:
+            idx = P["gidx"][P["own"]]
+            out.append(("p", idx, {f: a.comp[f][idx] for f in ("pF", "pf", "pm")}))
+        for C in a.C:
+            idx, idx1 = C["gidx"][C["own"]], C["gidx1"][C["own1"]]
+            out.append(("c", (idx, idx1), {"u": a.comp["u"][:, idx], "p": a.comp["p"][idx1]}))
+        conn.send((out, el))
+    conn.close()
+
+
+class OraclePool:
+    """The oracle's Algorithm 3 on a pool of worker processes (one per host core): positions split LPT-like by
+    box size, each worker marching its own coarse step (redundant, like the GPU ranks) and its subdomains; the
+    parent merges the owned core values (Step 4) into the composite and sends it back (mode B)."""
+
+    def __init__(self, cfg: dict, workers: int):
+        import multiprocessing as mp
+        from oracle import alg3
+        self.cfg = cfg
+        npos = int(np.prod(cfg["grid"]))
+        workers = max(1, min(workers, npos))
+        share = [list(range(w, npos, workers)) for w in range(workers)]
+        self.comp = alg3.Alg3(cfg, positions=[]).fields()
+        ctx = mp.get_context("fork")
+        self.conns, self.procs = [], []
+        for sh in share:
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_oracle_worker, args=(b, cfg, sh), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        for c in self.conns:
+            assert c.recv() == "ready"
+        self.workers = workers
+
+    def step(self) -> tuple[float, float]:
+        """One step; returns (wall seconds, fine-stage seconds = max over the workers + the merge)."""
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(self.comp)
+        new = {k: np.copy(v) for k, v in self.comp.items()}
+        fine = 0.0
+        outs = []
+        for c in self.conns:
+            out, el = c.recv()
+            fine = max(fine, el)
+            outs.append(out)
+        t1 = time.perf_counter()
+        for out in outs:
+            for kind, idx, vals in out:
+                if kind == "p":
+                    for f, v in vals.items():
+                        new[f][idx] = v
+                else:
+                    new["u"][:, idx[0]] = vals["u"]
+                    new["p"][idx[1]] = vals["p"]
+        self.comp = new
+        t2 = time.perf_counter()
+        return t2 - t0, fine + (t2 - t1)
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(timeout=10)
+
+
+def host_cores() -> tuple[int, str]:
+    n = len(os.sched_getaffinity(0))
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return n, model
+
+
+def oracle_measure(cfgi: int, warmup: int, steps: int, budget_s: float) -> dict:
+    """Fine-stage throughput of the pooled oracle (T_fine covers Steps 3-4, the coarse
+    trajectory is timed apart); the run stops after `steps` timed steps or when the wall time of the timed steps
+    exceeds budget_s (at least one step)."""
+    cfg, what = oracle_sample_cfg(cfgi)
+    cores, model = host_cores()
+    pool = OraclePool(cfg, cores)
+    try:
+        for _ in range(warmup):
+            pool.step()
+        fine, wall = [], []
+        while len(fine) < steps and (not wall or sum(wall) < budget_s):
+            w, f = pool.step()
+            wall.append(w)
+            fine.append(f)
+    finally:
+        pool.close()
+    D = I.fine_dofs(cfg)
+    T = sum(fine)
+    return {"value": D * len(fine) / T, "unit": "fine DOF*steps/s", "cores": pool.workers, "kind": "oracle",
+            "steps": len(fine), "warmup": warmup, "ms_per_step": 1e3 * T / len(fine),
+            "wall_ms_per_step_incl_coarse": 1e3 * sum(wall) / len(wall),
+            "sample": f"{what}; {len(fine)} timed step(s) after {warmup} warm-up, construction excluded; fine stage "
+                      f"(Steps 3-4: max over workers + merge), the redundant per-worker coarse step timed apart "
+                      f"(wall incl. coarse {sum(wall) / len(wall):.1f} s/step); {pool.workers} worker processes "
+                      f"(1 BLAS thread each) on {cores} host cores ({model}); SciPy SuperLU per subdomain"}
+
+
+def cpu_baseline(cfgi: int) -> dict:
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload (one step)."""
+    return oracle_measure(cfgi, warmup=0, steps=1, budget_s=20.0)
 
 
 def run_reference(args):
@@ -136,36 +270,19 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = I.config(args.config)
-    D = I.fine_dofs(cfg)
-    from oracle import alg3
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    a = alg3.Alg3(cfg)
-    budget = 120.0
-    times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        a.step()
-        el = time.perf_counter() - t0
-        if i >= args.warmup:
-            times.append(el)
-        if sum(times) > budget or (i + 1) >= cfg["steps"] and False:
-            break
-        if i + 1 >= cfg["steps"] + args.warmup:
-            break
-    T = sum(times) if times else float("nan")
-    k = len(times)
-    value = D * k / T if k else 0.0
-    sample = f"{cfg['name']}: {k} timed steps after {args.warmup} warm-up (oracle, SciPy SuperLU, 1 process)"
-    print(json.dumps({"impl": "reference", "metric": METRIC, "value": value, "unit": "fine DOF*steps/s",
-                      "n_gpus": args.gpus, "steps": k, "warmup": args.warmup,
-                      "ms_per_step": 1e3 * T / max(k, 1), "higher_is_better": True, "scaling": "strong",
+    m = oracle_measure(args.config, warmup=0, steps=args.steps, budget_s=120.0)
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": m["value"], "unit": "fine DOF*steps/s",
+                      "n_gpus": args.gpus, "steps": m["steps"], "warmup": m["warmup"],
+                      "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "strong",
                       "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                       "config": {"workload": cfg["name"], "dim": cfg["dim"], "H": cfg["H"], "h": cfg["h"],
-                                 "grid": cfg["grid"], "dt": cfg["dt"]},
-                      "cpu_baseline": {"value": value, "unit": "fine DOF*steps/s", "cores": 1, "kind": "oracle",
-                                       "sample": sample},
-                      "e2e": {"value": value, "unit": "fine DOF*steps/s", "h2d_bytes_per_step": 0,
+                                 "grid": cfg["grid"], "dt": cfg["dt"], "problem": cfg["problem"]},
+                      "cpu_baseline": {k: m[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                      "e2e": {"value": m["value"], "unit": "fine DOF*steps/s", "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0}}))
+
+
+L2_BYTES = 126e6
 
 
 def main():
@@ -247,9 +364,14 @@ def main():
         traffic_src = tr["source"]
     except Exception:
         traffic_src = None
-    roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    # regime (SURVEY 8(d) consequence 1): the rank's matrices (conduit: 12 B/nnz; porous: 3 x 8 + 4 B/nnz)
+    # against the 126 MB L2.  L2-resident families are labelled "l2": their algorithmic GB/s is an L2 rate and
+    # the ncu traffic beside it (dram bytes) shows how little reaches HBM.
+    mat_bytes = 12.0 * st1["nnz"][1] + 28.0 * st1["nnz"][0]
+    regime = "hbm" if mat_bytes > L2_BYTES else "l2"
+    roof = {"kernel": name, "bound": regime, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
-            "share_of_step": t / ms if ms > 0 else None,
+            "share_of_step": t / ms if ms > 0 else None, "matrix_bytes_rank": mat_bytes,
             "algorithmic_bytes_per_launch": b / max(n, 1), "ms_per_launch": t / max(n, 1)}
     out = {
         "metric": METRIC, "value": value, "unit": "fine DOF*steps/s", "n_gpus": world, "steps": args.steps,
@@ -305,10 +427,13 @@ def main():
             d2h += sum(v.nbytes for v in f.values())
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        h2d = (0 if cfg.get("k_mult") is None else np.asarray(cfg["k_mult"]).nbytes) + 8 * 64
+        s2 = sim2.stats()  # every host<->device copy the library made (create, steps, fields), counted in the library
         out["e2e"] = {"value": D * args.steps / el, "unit": "fine DOF*steps/s",
-                      "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-                      "includes": "lpfem_create (setup, assembly) + K x (lpfem_step + lpfem_get_fields to host)",
+                      "h2d_bytes_per_step": s2["h2d_bytes"] // args.steps,
+                      "d2h_bytes_per_step": s2["d2h_bytes"] // args.steps,
+                      "fields_bytes_per_step": d2h // args.steps,
+                      "includes": "lpfem_create from host inputs (setup, assembly) + K x (lpfem_step + "
+                                  "lpfem_get_fields to host); bytes counted by the library (lpfem_stats)",
                       "create_ms": 1e3 * t_create, "steps_ms": 1e3 * (el - t_create)}
         sim2.close()
     # SpMV building block of the Krylov kernels (BASELINE metric "SpMV % HBM peak"): the conduit family's batched
@@ -324,7 +449,7 @@ def main():
         out["spmv"] = {"unavailable": str(e)[:120]}
     sim.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg)
+        out["cpu_baseline"] = cpu_baseline(args.config)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

@@ -21,7 +21,9 @@
  *    lpfem_last_error() returns a ctx-owned message valid until the next call.
  *  - One host thread per ctx.  Work is enqueued on lpfem_dist.cuda_stream (NULL =
  *    the legacy default stream).  lpfem_create/step/get_fields/destroy are
- *    collective over lpfem_dist.world ranks (one process per GPU).
+ *    collective over lpfem_dist.world ranks (one process per GPU with the NCCL
+ *    transport; with LPFEM_TRANSPORT_LOCAL all ranks live in one process and
+ *    are stepped by lpfem_step_group).
  *  - Field layout: global lexicographic order, x fastest.  P2 fields live on the
  *    (2N_0+1)x(2N_1+1)[x(2N_2+1)] half-grid of their region (porous or conduit),
  *    P1 (conduit pressure) on the (N_0+1)x... vertices; the velocity is d
@@ -86,12 +88,27 @@ typedef struct {
                            time); any other value than 0 or that length is LPFEM_EINVAL */
   double picard_rtol;   /* coarse NS: ||du||_2 <= rtol ||u||_2 (C11): 1e-13 */
   int picard_max;       /* 50 */
+  int world_invariant;  /* 0 (default): Krylov launch geometry (thread-block cluster sizes, hence the order of
+                           the dot-product reductions) chosen per rank for speed: fields agree across world
+                           sizes to the solver tolerance (C19), not bitwise.  1: chosen from the GLOBAL system
+                           counts, identical on every rank and for every world size, so the fields are bitwise
+                           identical for any world (cost: at world N a rank's Krylov launches
+                           use about 1/N of the SMs the per-rank choice would use) */
 } lpfem_opts;
+
+enum { LPFEM_TRANSPORT_NCCL = 0,    /* one process per GPU; halo exchange by NCCL grouped send/recv (default) */
+       LPFEM_TRANSPORT_LOCAL = 1    /* all ranks are contexts of ONE process (any devices, possibly the same one),
+                                       stepped together by lpfem_step_group; the exchange copies each peer's
+                                       packed send buffer (cudaMemcpyPeerAsync).  Same plan, pack/unpack and
+                                       gather code as the NCCL transport; used to run the multi-rank path on
+                                       a single GPU (tests) */ };
 
 typedef struct {
   int rank, world, device;
-  unsigned char nccl_id[128]; /* from lpfem_nccl_unique_id on rank 0, broadcast by the caller */
+  unsigned char nccl_id[128]; /* NCCL: from lpfem_nccl_unique_id on rank 0, broadcast by the caller.
+                                 LOCAL: any 128 bytes identifying the group (equal on all its ranks) */
   void* cuda_stream;          /* cudaStream_t or NULL */
+  int transport;              /* LPFEM_TRANSPORT_* */
 } lpfem_dist;
 
 typedef struct {
@@ -111,6 +128,12 @@ typedef struct {
   long long krylov_launches[2];    /* number of fine Krylov launches */
   long long coarse_factorizations; /* cumulative dense LU factorisations of the coarse Navier-Stokes Jacobian
                                       (chord iteration reuses the last one while it contracts) */
+  double t_coarse_part_ms[3];      /* t_coarse_ms by part: [porous solves, Navier-Stokes chord/Picard iteration,
+                                      coarse-box inverses of the multilevel preconditioner] (elapsed on the
+                                      coarse stream; overlapped with the fine stage unless LPFEM_NO_OVERLAP) */
+  long long h2d_bytes, d2h_bytes;  /* cumulative host->device / device->host bytes copied by this library
+                                      (create: tables, patterns, k_mult; step: solver statistics, coarse
+                                      Picard norms; get_fields: the fields when on_device = 0) */
 } lpfem_stats;
 
 /* NCCL unique id for a multi-GPU ctx (rank 0 only; world > 1). */
@@ -126,21 +149,41 @@ lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs
                           double H, double h, double overlap, const int subdomain_grid[3],
                           const lpfem_opts* opts, const lpfem_dist* dist, lpfem_ctx** out);
 
-/* One step t_n -> t_{n+1} = (n+1) dt (C18): coarse step, fine corrections on
+/* One step t_n -> t_{n+1} (C18: t_{n+1} = t_b + (n+1-n_b) dt, with (n_b, t_b) the step and time at which the
+ * current dt took effect, i.e. (n+1) dt when dt never changes): coarse step, fine corrections on
  * every local subdomain, write-back and halo exchange.  A change
- * of dt re-assembles the porous operators.  On LPFEM_ENOCONV the state stays at t_n.  Collective.
+ * of dt re-assembles the dt-dependent operators.  Collective (world > 1: the convergence verdict is reduced
+ * over the ranks, so all ranks commit or none does).
+ * Commit semantics: the write-back goes to shadow composite arrays (and, in mode A, shadow corrections) that
+ * replace the state only when every Krylov solve of every rank met C19 and the coarse step converged (C11).
+ * On LPFEM_ENOCONV nothing is committed: lpfem_get_fields still returns t_n, lpfem_get_stats().steps is
+ * unchanged, and the call may be repeated (e.g. with a smaller dt).  A non-converged coarse step that was
+ * computed ahead on the side stream is reported by the step that consumes it.  Iteration and timing counters
+ * in lpfem_stats are cumulative over all attempts.
  * The coarse step for t_{n+2} is computed on a side stream while this call's fine stage runs (it is
  * waited for at the next call); the fine Krylov solves start from the previous steps' corrections
  * (same stopping test, C19); the coarse Navier-Stokes solve is a chord iteration on the last factorised
  * Jacobian (same C11 test).  None of these changes the discrete solution beyond the stated tolerances. */
 lpfem_status lpfem_step(lpfem_ctx* ctx, double dt);
 
+/* lpfem_step for the ranks of one LPFEM_TRANSPORT_LOCAL group, stepped together from one host thread:
+ * ctxs[0..n-1] are all `world` contexts of the group (any order).  Same semantics as lpfem_step on each
+ * (the convergence verdict is the AND over the group).  LPFEM_EINVAL if the contexts do not form one complete
+ * local group. */
+lpfem_status lpfem_step_group(lpfem_ctx* const* ctxs, int n, double dt);
+
+/* Fault injection (test hook, SURVEY 5 "failure detection"): cap the Krylov iterations of every later fine
+ * solve of `family` (0 porous PCG, 1 conduit GMRES) at max_iter (> 0), so that the next steps fail with
+ * LPFEM_ENOCONV; max_iter <= 0 removes the cap.  The coarse solves keep lpfem_opts.max_iter. */
+lpfem_status lpfem_inject_fault(lpfem_ctx* ctx, int family, int max_iter);
+
 /* Node counts of the global fine fields: [porous, conduit]. */
 lpfem_status lpfem_get_sizes(const lpfem_ctx* ctx, long long n_nodes_p2[2], long long n_nodes_p1[2]);
 
 /* Copy the composite fine fields at t_n: pF, pf, pm (n_p2[0] each), u (dim * n_p2[1], SoA), p (n_p1[1]).
  * on_device = 1: the pointers are device pointers on this ctx's GPU; 0: host pointers.  The
- * owned values of all ranks are gathered on `root` (other ranks may pass NULL).  Collective. */
+ * owned values of all ranks are gathered on `root` (other ranks may pass NULL).  Collective with the NCCL
+ * transport; with LPFEM_TRANSPORT_LOCAL only the root's call is needed (it reads its peers' arrays). */
 lpfem_status lpfem_get_fields(lpfem_ctx* ctx, double* pF, double* pf, double* pm, double* u, double* p,
                               int on_device, int root);
 
@@ -179,14 +222,20 @@ lpfem_status lpfem_get_system(lpfem_ctx* ctx, int family, int local_index, int f
 lpfem_status lpfem_bench_spmv(lpfem_ctx* ctx, int family, int reps, int flush, double* ms_per_rep,
                               double* bytes_per_rep);
 
-/* Multi-GPU plan (host only, no device needed): subdomain positions are split into contiguous
- * blocks over `world` ranks; a fine node belongs to the rank of its owning subdomain (C3).  For one region
- * meshed with n_cells fine cells per axis, returns global node indices (P2 half-grid lexicographic, or P1
- * vertex lexicographic if vertex_only): kind 0 = nodes owned by `peer` that `rank` reads (its halo),
- * 1 = nodes owned by `rank` that `peer` reads, 2 = all nodes owned by `peer`.  Sorted, unique.  out may be
- * NULL to query the count. */
-lpfem_status lpfem_halo_plan(int dim, const int n_cells[3], const int subdomain_grid[3], int overlap_cells, int rank,
-                             int world, int vertex_only, int kind, int peer, int* out, long long* n_out);
+/* Multi-GPU placement (host only, no device needed): rank_of_pos[s] for every subdomain position
+ * s (lexicographic in the subdomain grid): LPT on the cell counts of the extended porous + conduit boxes
+ * (csrc/halo.h).  n_cells_p / n_cells_c: fine cells per axis of the porous / conduit region. */
+lpfem_status lpfem_placement(int dim, const int n_cells_p[3], const int n_cells_c[3], const int subdomain_grid[3],
+                             int overlap_cells, int world, int* rank_of_pos);
+
+/* Multi-GPU halo plan (host only): a fine node belongs to the rank of its owning subdomain (C3) under
+ * lpfem_placement.  For region `region` (0 porous, 1 conduit), returns global node indices (P2 half-grid
+ * lexicographic, or P1 vertex lexicographic if vertex_only): kind 0 = nodes owned by `peer` that `rank` reads
+ * (its halo), 1 = nodes owned by `rank` that `peer` reads, 2 = all nodes owned by `peer`.  Sorted, unique.
+ * out may be NULL to query the count. */
+lpfem_status lpfem_halo_plan(int dim, const int n_cells_p[3], const int n_cells_c[3], const int subdomain_grid[3],
+                             int overlap_cells, int region, int rank, int world, int vertex_only, int kind, int peer,
+                             int* out, long long* n_out);
 
 const char* lpfem_last_error(const lpfem_ctx* ctx);
 const char* lpfem_status_string(lpfem_status s);

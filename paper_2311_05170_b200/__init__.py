@@ -27,9 +27,11 @@ LAG = {"composite": 0, "subdomain": 1}
 STATUS = ["ok", "einval", "enotdiv", "emisalign", "enoconv", "ecuda", "enccl", "enomem", "estate"]
 
 # Exported symbols (kept in sync with include/lpfem.h; checked by tests/test_abi.py)
-SYMBOLS = ["lpfem_nccl_unique_id", "lpfem_create", "lpfem_step", "lpfem_get_sizes", "lpfem_get_fields",
-           "lpfem_get_coarse_fields", "lpfem_get_mesh", "lpfem_get_layout", "lpfem_get_stats", "lpfem_get_system",
-           "lpfem_halo_plan", "lpfem_last_error", "lpfem_status_string", "lpfem_destroy", "lpfem_bench_spmv"]
+SYMBOLS = ["lpfem_nccl_unique_id", "lpfem_create", "lpfem_step", "lpfem_step_group", "lpfem_inject_fault",
+           "lpfem_get_sizes", "lpfem_get_fields", "lpfem_get_coarse_fields", "lpfem_get_mesh", "lpfem_get_layout",
+           "lpfem_get_stats", "lpfem_get_system", "lpfem_placement", "lpfem_halo_plan", "lpfem_last_error",
+           "lpfem_status_string", "lpfem_destroy", "lpfem_bench_spmv"]
+TRANSPORT = {"nccl": 0, "local": 1}
 
 
 class Geometry(C.Structure):
@@ -49,12 +51,12 @@ class Data(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("lag_mode", C.c_int), ("krylov_rtol", C.c_double), ("max_iter", C.c_int), ("gmres_restart", C.c_int),
-                ("picard_rtol", C.c_double), ("picard_max", C.c_int)]
+                ("picard_rtol", C.c_double), ("picard_max", C.c_int), ("world_invariant", C.c_int)]
 
 
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("device", C.c_int), ("nccl_id", C.c_ubyte * 128),
-                ("cuda_stream", C.c_void_p)]
+                ("cuda_stream", C.c_void_p), ("transport", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -64,7 +66,8 @@ class Stats(C.Structure):
                 ("n_systems", C.c_longlong * 2), ("n_rows", C.c_longlong * 2), ("nnz", C.c_longlong * 2),
                 ("fine_dofs", C.c_longlong), ("kernel_launches", C.c_longlong),
                 ("t_krylov_ms", C.c_double * 2), ("bytes_krylov", C.c_double * 2),
-                ("krylov_launches", C.c_longlong * 2), ("coarse_factorizations", C.c_longlong)]
+                ("krylov_launches", C.c_longlong * 2), ("coarse_factorizations", C.c_longlong),
+                ("t_coarse_part_ms", C.c_double * 3), ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong)]
 
 
 class LPFEMError(RuntimeError):
@@ -87,6 +90,9 @@ def lib() -> C.CDLL:
         L.lpfem_create.argtypes = [P(Geometry), P(Coeffs), P(Data), C.c_double, C.c_double, C.c_double,
                                    P(C.c_int), P(Opts), P(Dist), P(C.c_void_p)]
         L.lpfem_step.argtypes = [C.c_void_p, C.c_double]
+        L.lpfem_step_group.argtypes = [P(C.c_void_p), C.c_int, C.c_double]
+        L.lpfem_inject_fault.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.lpfem_placement.argtypes = [C.c_int, P(C.c_int), P(C.c_int), P(C.c_int), C.c_int, C.c_int, C.c_void_p]
         L.lpfem_get_sizes.argtypes = [C.c_void_p, P(C.c_longlong), P(C.c_longlong)]
         L.lpfem_get_fields.argtypes = [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int, C.c_int]
         L.lpfem_get_coarse_fields.argtypes = [C.c_void_p] + [C.c_void_p] * 5
@@ -102,8 +108,8 @@ def lib() -> C.CDLL:
         L.lpfem_status_string.restype = C.c_char_p
         L.lpfem_destroy.argtypes = [C.c_void_p]
         L.lpfem_nccl_unique_id.argtypes = [C.c_void_p]
-        L.lpfem_halo_plan.argtypes = [C.c_int, P(C.c_int), P(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                                      C.c_int, C.c_void_p, P(C.c_longlong)]
+        L.lpfem_halo_plan.argtypes = [C.c_int, P(C.c_int), P(C.c_int), P(C.c_int), C.c_int, C.c_int, C.c_int,
+                                      C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, P(C.c_longlong)]
         _LIB = L
     return _LIB
 
@@ -116,7 +122,8 @@ class LPFEM:
     """One context (one GPU, one rank).  cfg: a dict from ``lpfem_inputs.config``."""
 
     def __init__(self, cfg: dict, rank: int = 0, world: int = 1, device: int = 0, stream: int | None = None,
-                 nccl_id: bytes | None = None, max_iter: int = 20000):
+                 nccl_id: bytes | None = None, max_iter: int = 20000, transport: str = "nccl",
+                 world_invariant: bool = False):
         L = lib()
         d = cfg["dim"]
         g = Geometry(dim=d)
@@ -137,8 +144,8 @@ class LPFEM:
                    const_value=cfg.get("const_value", 1.0))
         o = Opts(lag_mode=LAG[cfg.get("lag_mode", "composite")], krylov_rtol=cfg.get("krylov_rtol", 1e-12),
                  max_iter=max_iter, gmres_restart=0, picard_rtol=cfg.get("picard_rtol", 1e-13),
-                 picard_max=cfg.get("picard_max", 50))
-        ds = Dist(rank=rank, world=world, device=device, cuda_stream=stream)
+                 picard_max=cfg.get("picard_max", 50), world_invariant=int(world_invariant))
+        ds = Dist(rank=rank, world=world, device=device, cuda_stream=stream, transport=TRANSPORT[transport])
         if nccl_id is not None:
             C.memmove(ds.nccl_id, nccl_id, 128)
         grid = (C.c_int * 3)(*(list(cfg["grid"]) + [1] * (3 - d)))
@@ -162,6 +169,10 @@ class LPFEM:
 
     def step(self, dt: float | None = None):
         self._check(lib().lpfem_step(self._h, self.cfg["dt"] if dt is None else dt))
+
+    def inject_fault(self, family: int, max_iter: int):
+        """Test hook (lpfem_inject_fault): cap the fine Krylov iterations of family 0 (porous) / 1 (conduit)."""
+        self._check(lib().lpfem_inject_fault(self._h, family, max_iter))
 
     def fields(self) -> dict:
         """Composite fine fields at t_n as host numpy arrays (global lexicographic, x fastest)."""
@@ -263,17 +274,65 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def _i3(v, dim):
+    return (C.c_int * 3)(*(list(v) + [1] * (3 - dim)))
+
+
+def placement(dim: int, n_cells_p, n_cells_c, grid, overlap_cells: int, world: int) -> np.ndarray:
+    """lpfem_placement: rank of every subdomain position (LPT on box cells, csrc/halo.h)."""
+    out = np.empty(int(np.prod(grid)), np.int32)
+    st = lib().lpfem_placement(dim, _i3(n_cells_p, dim), _i3(n_cells_c, dim), _i3(grid, dim), overlap_cells, world,
+                               _ptr(out))
+    if st != 0:
+        raise LPFEMError(st, "lpfem_placement")
+    return out
+
+
 def halo_plan(dim: int, n_cells, grid, overlap_cells: int, rank: int, world: int, kind: str, peer: int,
-              vertex_only: bool = False) -> np.ndarray:
-    """Host-side multi-GPU plan (lpfem_halo_plan): kind "need" | "give" | "owned"."""
+              vertex_only: bool = False, region: int = 0, n_cells_other=None) -> np.ndarray:
+    """Host-side multi-GPU plan (lpfem_halo_plan) of one region: kind "need" | "give" | "owned".  n_cells: the
+    region's fine cells per axis; n_cells_other: the other region's (default: the same)."""
     L = lib()
     k = {"need": 0, "give": 1, "owned": 2}[kind]
-    nc = (C.c_int * 3)(*(list(n_cells) + [1] * (3 - dim)))
-    gr = (C.c_int * 3)(*(list(grid) + [1] * (3 - dim)))
+    other = n_cells if n_cells_other is None else n_cells_other
+    ncp, ncc = (n_cells, other) if region == 0 else (other, n_cells)
+    args = (dim, _i3(ncp, dim), _i3(ncc, dim), _i3(grid, dim), overlap_cells, region, rank, world, int(vertex_only),
+            k, peer)
     n = C.c_longlong()
-    st = L.lpfem_halo_plan(dim, nc, gr, overlap_cells, rank, world, int(vertex_only), k, peer, None, C.byref(n))
+    st = L.lpfem_halo_plan(*args, None, C.byref(n))
     if st != 0:
         raise LPFEMError(st, "lpfem_halo_plan")
     out = np.empty(n.value, np.int32)
-    L.lpfem_halo_plan(dim, nc, gr, overlap_cells, rank, world, int(vertex_only), k, peer, _ptr(out), C.byref(n))
+    L.lpfem_halo_plan(*args, _ptr(out), C.byref(n))
     return out
+
+
+class LocalGroup:
+    """All `world` ranks of the multi-rank path as contexts of THIS process (LPFEM_TRANSPORT_LOCAL), stepped
+    together by lpfem_step_group: same placement, halo plan, pack/unpack and gather code as the NCCL transport,
+    runnable on one GPU (tests).  fields() gathers on rank 0."""
+
+    _next_key = 0
+
+    def __init__(self, cfg: dict, world: int, device: int = 0, world_invariant: bool = False, **kw):
+        LocalGroup._next_key += 1
+        key = f"lpfem-local-{os.getpid()}-{LocalGroup._next_key}".encode().ljust(128, b"\0")
+        self.cfg = cfg
+        self.ranks = [LPFEM(cfg, rank=r, world=world, device=device, nccl_id=key, transport="local",
+                            world_invariant=world_invariant, **kw) for r in range(world)]
+
+    def step(self, dt: float | None = None):
+        arr = (C.c_void_p * len(self.ranks))(*[r._h.value for r in self.ranks])
+        st = lib().lpfem_step_group(arr, len(self.ranks), self.cfg["dt"] if dt is None else dt)
+        if st != 0:
+            raise LPFEMError(st, lib().lpfem_last_error(self.ranks[0]._h).decode())
+
+    def fields(self) -> dict:
+        return self.ranks[0].fields()
+
+    def stats(self) -> list:
+        return [r.stats() for r in self.ranks]
+
+    def close(self):
+        for r in self.ranks:
+            r.close()

@@ -31,6 +31,24 @@ struct KSys {
   long long val_off;   // values: offset added to rowptr positions
   int nrows;
   int pad;
+  long long item_off;  // node-blocked conduit format: first item (velocity node / pressure vertex) of the system
+  int n2, n1;          // P2 nodes and P1 vertices of the system (conduit)
+};
+
+// Node-blocked conduit operator (fine Taylor-Hood systems): the D velocity rows of a P2 node share one column
+// list, so they are stored together.  Item k of a system is velocity node k (k < n2) or pressure vertex k - n2.
+//   node:   cols [L P2 neighbours (local P2 index) | L1 P1 neighbours (local P1 index)]; values: the node's D rows
+//           consecutively, row a = [b = 0 block (L) | ... | b = D-1 block (L) | P1 block (L1)]  (the CSR row a
+//           of the node, unchanged)
+//   vertex: cols [L P2 neighbours]; values: the continuity row [b = 0 block (L) | ... | b = D-1 block]
+// Per nonzero 8 B of value and, per (node, neighbour) pair, 4 B of column shared by the D x D block (the CSR
+// stores 4 B per nonzero): 12 -> ~8.5 B per nonzero in 3D.
+struct NBMat {
+  const double* val;
+  const int* col;
+  const long long* vptr;  // per item (family item space): first value
+  const long long* cptr;  // per item: first column
+  const int2* len;        // per item: (L, L1)
 };
 
 struct KStat {
@@ -95,6 +113,9 @@ struct KArgs {
   int warm;          // 1: x holds the previous step's solution of the same system, used as the initial guess;
                      // 2: also xp holds the one before: initial guess 2 x - xp (linear extrapolation in time)
   double* xp;        // warm == 2: the solution two steps back (updated to the previous one)
+  NBMat nb;          // GMRES: node-blocked operator (nb.val != NULL), else the CSR (rowptr, col, val)
+  const int* order;  // NULL, or the system of each cluster in launch order (clusters are dispatched in index
+                     // order: the systems expected to take longest start first, LPT; no effect on the numbers)
 };
 
 // Sparsity pattern of the CTA's rows [r0, r1): staged once per solve in dynamic shared memory when it fits (the
@@ -365,6 +386,91 @@ __device__ __forceinline__ void spmv(const CtaPattern& P, const double* __restri
     spmv_rows<NT, TPR>(P.rp, P.col, P.val, x, y, r0, r1);
 }
 
+// y = A x over the items [i0, i1) of one system (node-blocked format), TPR lanes per item; y rows of node i are
+// a n2 + i, of vertex k: D n2 + k.  The lanes of an item walk its neighbours; per neighbour one column load, D
+// (node) x gathers and D^2 value loads, all independent.
+template <int NT, int TPR, int D>
+__device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int n2, const double* __restrict__ x,
+                                        double* __restrict__ y, int i0, int i1) {
+  constexpr int NG = NT / TPR;
+  const int lane = threadIdx.x % TPR;
+  for (int base = i0; base < i1; base += NG) {
+    const int it = base + threadIdx.x / TPR;
+    double acc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) acc[a] = 0.0;
+    const bool node = it < n2;
+    if (it < i1) {
+      const long long g = item_off + it;
+      const int2 ln = B.len[g];
+      const double* v = B.val + B.vptr[g];
+      const int* cl = B.col + B.cptr[g];
+      const int L = ln.x, L1 = ln.y;
+      if (node) {
+        const int rl = D * L + L1;  // row length
+        for (int k = lane; k < L; k += TPR) {
+          const int c = __ldg(cl + k);
+          double xb[D], vv[D][D];
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) vv[a][bb] = __ldg(v + a * rl + bb * L + k);
+#pragma unroll
+          for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) acc[a] += vv[a][bb] * xb[bb];
+        }
+        for (int k = lane; k < L1; k += TPR) {
+          const int c = __ldg(cl + L + k);
+          double vv[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) vv[a] = __ldg(v + a * rl + D * L + k);
+          const double xp = x[D * n2 + c];
+#pragma unroll
+          for (int a = 0; a < D; ++a) acc[a] += vv[a] * xp;
+        }
+      } else {
+        for (int k = lane; k < L; k += TPR) {
+          const int c = __ldg(cl + k);
+          double vv[D], xb[D];
+#pragma unroll
+          for (int bb = 0; bb < D; ++bb) vv[bb] = __ldg(v + bb * L + k);
+#pragma unroll
+          for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
+#pragma unroll
+          for (int bb = 0; bb < D; ++bb) acc[0] += vv[bb] * xb[bb];
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int o = TPR / 2; o > 0; o >>= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o, TPR);
+    if (it < i1 && lane == 0) {
+      if (node) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) y[a * n2 + it] = acc[a];
+      } else {
+        y[D * n2 + (it - n2)] = acc[0];
+      }
+    }
+  }
+}
+
+// Standalone batched node-blocked SpMV over every system of the conduit family (lpfem_bench_spmv)
+template <int NT, int TPR, int D>
+__global__ void __launch_bounds__(NT) k_spmv_nb_family(const KSys* __restrict__ sys, NBMat B,
+                                                       const double* __restrict__ x, double* __restrict__ y,
+                                                       int items_per_cta) {
+  const KSys K = sys[blockIdx.y];
+  const int i0 = blockIdx.x * items_per_cta;
+  if (i0 >= K.n2 + K.n1) return;
+  const int i1 = min(K.n2 + K.n1, i0 + items_per_cta);
+  spmv_nb<NT, TPR, D>(B, K.item_off, K.n2, x + K.row_off, y + K.row_off, i0, i1);
+}
+
 // bytes of the GMRES(M) Hessenberg matrix (M + 1) x M in dynamic shared memory, 16-byte aligned
 __host__ __device__ constexpr int gmres_h_bytes(int M) { return (((M + 1) * M * 8) + 15) & ~15; }
 
@@ -392,7 +498,7 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int CL = (int)cl.num_blocks();
   const int crank = (int)cl.block_rank();
-  const int sid = blockIdx.x / CL;
+  const int sid = A.order ? A.order[blockIdx.x / CL] : blockIdx.x / CL;  // launch order: most work first
   const KSys K = A.sys[sid];
   const int chunk = (K.nrows + CL - 1) / CL;
   const int r0 = min(K.nrows, crank * chunk), r1 = min(K.nrows, r0 + chunk);
@@ -655,7 +761,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
   cgx::cluster_group cl = cgx::this_cluster();
   const int CL = (int)cl.num_blocks();
   const int crank = (int)cl.block_rank();
-  const int sid = blockIdx.x / CL;
+  const int sid = A.order ? A.order[blockIdx.x / CL] : blockIdx.x / CL;  // launch order: most work first
   const KSys K = A.sys[sid];
   const int chunk = (K.nrows + CL - 1) / CL;
   const int r0 = min(K.nrows, crank * chunk), r1 = min(K.nrows, r0 + chunk);
@@ -840,7 +946,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int CL = (int)cl.num_blocks();
   const int crank = (int)cl.block_rank();
-  const int sid = blockIdx.x / CL;
+  const int sid = A.order ? A.order[blockIdx.x / CL] : blockIdx.x / CL;  // launch order: most work first
   const KSys K = A.sys[sid];
   const int chunk = (K.nrows + CL - 1) / CL;
   const int r0 = min(K.nrows, crank * chunk), r1 = min(K.nrows, r0 + chunk);
@@ -858,6 +964,20 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   extern __shared__ __align__(16) double lp_gdyn[];
   double(*H)[M] = reinterpret_cast<double(*)[M]>(lp_gdyn);
   const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1, gmres_h_bytes(M));
+  // node-blocked operator: the CTA's items (velocity nodes, then pressure vertices) instead of its rows; the
+  // product then spans other CTAs' rows, so it ends with a cluster barrier
+  const bool nbk = A.nb.val != nullptr;
+  const int nitems = K.n2 + K.n1, ichunk = (nitems + CL - 1) / CL;
+  const int it0 = min(nitems, crank * ichunk), it1 = min(nitems, it0 + ichunk);
+  auto matvec = [&](const double* X, double* Y) {
+    if (nbk) {
+      spmv_nb<NT, TPR, D>(A.nb, K.item_off, K.n2, X, Y, it0, it1);
+      cl.sync();
+    } else {
+      spmv<NT, TPR, D == 2>(PT, X, Y, r0, r1);
+      __syncthreads();
+    }
+  };
   __shared__ RedSmem<NT, M + 2> S;
   __shared__ double cs[M], sn[M], gv[M + 1], yv[M], hc[M + 1], sig[M + 1], hs[M + 1];
   int par = 0;
@@ -892,8 +1012,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     for (int i = r0 + tid; i < r1; i += NT) x[i] = 0.0;
   } else if (A.warm) {
     // initial guess: the previous step's correction (the stopping test stays ||b - A x|| <= rtol ||b||, C19)
-    spmv<NT, TPR, D == 2>(PT, x, W, r0, r1);
-    __syncthreads();
+    matvec(x, W);
     double pr = 0.0;
     for (int i = r0 + tid; i < r1; i += NT) {
       const double ri = b[i] - W[i];
@@ -924,11 +1043,10 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);
-        spmv<NT, TPR, D == 2>(PT, Zw, W, r0, r1);
+        matvec(Zw, W);
       } else {
-        spmv<NT, TPR, D == 2>(PT, V + j * ld, W, r0, r1);
+        matvec(V + j * ld, W);
       }
-      __syncthreads();
       PHASE(2);
       // w = sj * W;  pass A: h_k = sig_k Vt_k^T w and ||w||^2
       double pw = 0.0;
@@ -1029,8 +1147,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     }
     cl.sync();
     ++nspmv;
-    spmv<NT, TPR, D == 2>(PT, x, W, r0, r1);
-    __syncthreads();
+    matvec(x, W);
     double pr = 0.0;
     for (int i = r0 + tid; i < r1; i += NT) {
       const double ri = b[i] - W[i];

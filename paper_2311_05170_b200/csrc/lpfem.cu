@@ -16,6 +16,9 @@
 #include <string>
 #include <vector>
 
+#include <map>
+#include <mutex>
+
 #include <cub/device/device_scan.cuh>
 #include <cusolverDn.h>
 #include <nccl.h>
@@ -46,6 +49,25 @@ struct Err : std::runtime_error {
   } while (0)
 
 thread_local long long tl_launches = 0;  // kernel launches of this library (host thread of the ctx)
+// host<->device bytes moved by this library (host thread of the ctx): lpfem_stats.h2d_bytes / d2h_bytes
+thread_local long long tl_h2d = 0, tl_d2h = 0;
+inline void count_copy(size_t n, cudaMemcpyKind k) {
+  if (k == cudaMemcpyHostToDevice) tl_h2d += (long long)n;
+  if (k == cudaMemcpyDeviceToHost) tl_d2h += (long long)n;
+}
+inline cudaError_t cpy(void* d, const void* s, size_t n, cudaMemcpyKind k) {
+  count_copy(n, k);
+  return cudaMemcpy(d, s, n, k);
+}
+inline cudaError_t cpya(void* d, const void* s, size_t n, cudaMemcpyKind k, cudaStream_t st) {
+  count_copy(n, k);
+  return cudaMemcpyAsync(d, s, n, k, st);
+}
+template <class T>
+cudaError_t cpysym(const T& sym, const void* s, size_t n) {
+  tl_h2d += (long long)n;
+  return cudaMemcpyToSymbol(sym, s, n);
+}
 #define CKL()                      \
   do {                             \
     CK(cudaGetLastError());        \
@@ -92,6 +114,7 @@ struct NcclApi {
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
   bool load() {
     if (h) return true;
     h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -104,7 +127,8 @@ struct NcclApi {
     groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
     groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
     errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-    return getUniqueId && commInitRank && commDestroy && send && recv && groupStart && groupEnd && errStr;
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    return getUniqueId && commInitRank && commDestroy && send && recv && groupStart && groupEnd && errStr && allReduce;
   }
 };
 NcclApi g_nccl;
@@ -139,11 +163,22 @@ struct Family {
   // vectors
   double *base = nullptr, *z = nullptr, *lag = nullptr, *qf = nullptr, *aux = nullptr, *W = nullptr;
   double *rhs = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *V = nullptr, *ecorr = nullptr;
+  double* ecorr2 = nullptr;  // mode A: corrections of the step being computed (committed by swapping with ecorr)
   std::vector<KSys> hk;
   KSys* dk = nullptr;
   KStat* dstat = nullptr;
   std::vector<KStat> hstat;
+  // node-blocked copy of the fine conduit operator (krylov.cuh NBMat), used by the GMRES SpMV
+  double* nbval = nullptr;
+  int* nbcol = nullptr;
+  long long *nbvptr = nullptr, *nbcptr = nullptr, *nbioff = nullptr;
+  int2* nblen = nullptr;
+  long long nb_items = 0, nb_ncols = 0;
+  std::vector<long long> h_ioff;
+  std::vector<int> order;        // fine Krylov launches: systems in decreasing expected work (rows x last iterations)
+  int* dorder = nullptr;
   int cluster = 1;
+  int nsys_rule = 1;             // system count the cluster rules use (local, or global with world_invariant)
   bool cluster_checked = false;  // cluster size reduced until all clusters are co-resident (resident_cluster)
   bool bandwidth_bound = false;  // large systems: keep the largest cluster even if the launch needs two waves
   int solved = 0;                // previous solutions held: x (>= 1), xp (>= 2) (Krylov warm start)
@@ -154,7 +189,8 @@ struct Family {
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
     void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, dinv, zv, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
-                    rhs, x, r, p, q, V, ecorr, dk, dstat, xp};
+                    rhs, x, r, p, q, V, ecorr, ecorr2, dk, dstat, xp, dorder, nbval, nbcol, nbvptr, nbcptr,
+                    nbioff, nblen};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
   }
@@ -185,6 +221,7 @@ struct lpfem_ctx {
   cudaEvent_t evp[3] = {};     // fork / join of st3; [2]: conduit GMRES about to launch (gates the porous PCG)
   bool gate = false;           // concurrent fine stage: record / wait evp[2] around the Krylov launches
   cudaEvent_t evc[3] = {};
+  cudaEvent_t evcp[2] = {};  // coarse step parts: after the porous solves, after the Navier-Stokes iteration
   long long coarse_n = 0;      // latest coarse time index available
   double coarse_dt = -1.0;
   bool overlap = true;
@@ -195,14 +232,26 @@ struct lpfem_ctx {
   cusolverDnHandle_t sol2 = nullptr;
   double *wpic = nullptr, *wpic2 = nullptr, *ppic = nullptr, *ppic2 = nullptr;
   double* nrm = nullptr;  // 2 doubles
-  // composite fine fields
+  // composite fine fields at t_n (committed state) and the shadow arrays the running step writes back into;
+  // the two sets are swapped when the step commits (lpfem_step: nothing is committed on LPFEM_ENOCONV)
   double* comp[3] = {};
   double* comp_u = nullptr;
   double* comp_p = nullptr;
+  double* comp2[3] = {};
+  double* comp2_u = nullptr;
+  double* comp2_p = nullptr;
+  // time levels (C18): t_{n+1} = t_base + (n + 1 - n_base) dt, (n_base, t_base) = where the current dt took effect
+  double t_now = 0.0, t_base = 0.0;
+  long long n_base = 0;
+  int fault_maxit[2] = {0, 0};  // lpfem_inject_fault: cap of the fine Krylov iterations (0 = none)
+  bool pending_ok = true;       // convergence verdict of the step in flight (step_begin .. step_end)
+  double pending_t = 0.0;
+  double pending_res[2] = {0, 0};
   long long n2p_f = 0, n2c_f = 0, n1c_f = 0, n2p_c = 0, n2c_c = 0, n1c_c = 0;
   double* kmult = nullptr;
   std::vector<double> hkmult;
   void* ref = nullptr;
+  void* convt = nullptr;  // ConvT<D>: per-simplex-type convection tensors (k_conduit_step_nb)
   cudaStream_t st = nullptr;
   cudaEvent_t ev[4] = {};
   cudaEvent_t ek[4] = {};
@@ -234,6 +283,14 @@ struct lpfem_ctx {
   double clu_dt = -1.0;
   double* lwk2 = nullptr;                // cuSOLVER workspace of sol2 (coarse stream)
   int *lpiv2 = nullptr, *linfo2 = nullptr;
+  // 3D coarse-box inverses: NSI concurrent cuSOLVER streams (one LU + solve-with-identity per box, round robin)
+  static constexpr int NSI = 8;
+  int nsi = 0;
+  cudaStream_t sinv[NSI] = {};
+  cusolverDnHandle_t hinv[NSI] = {};
+  double* lwki[NSI] = {};
+  int *lpivi[NSI] = {}, *linfoi[NSI] = {};
+  cudaEvent_t einv[NSI + 1] = {};
   long long *dpoff = nullptr, *daoff = nullptr;
   std::vector<long long> haoff;
   int *lpiv = nullptr, *linfo = nullptr;
@@ -250,12 +307,18 @@ struct lpfem_ctx {
   SysDesc* pds3 = nullptr;        // porous coarse-box descriptors, one per (field, box) system
   long long* daoff_p = nullptr;
   std::vector<long long> haoff_p;
-  // multi-GPU (world > 1): NCCL communicator, halo plan, exchange buffers
+  // multi-GPU (world > 1): NCCL communicator or local group, halo plan, exchange buffers
   ncclComm_t comm = nullptr;
   std::vector<PeerX> peers;
+  std::vector<int> rank_of_pos;  // placement of the subdomain positions (halo.h, LPT)
   HaloPlan plan_p, plan_c2, plan_c1;
-  double* gbuf = nullptr;  // gather buffer (root)
+  std::vector<int*> own_p, own_c2, own_c1;  // device copies of every rank's owned lists (gather to root)
+  double* gbuf = nullptr;  // gather buffer
   long long gbuf_n = 0;
+  int* dok = nullptr;            // NCCL: convergence verdict, min-reduced over the ranks
+  cudaEvent_t ev_pack = nullptr; // local transport: this rank's send buffers are packed
+  cudaEvent_t ev_xdone = nullptr;  // local transport: this rank's copies out of its peers' buffers are done
+  std::string group_key;         // local transport: registry key (dist.nccl_id bytes)
   // coarse Navier-Stokes: dense LU on the device (cuSOLVER), Step 1 dependency (C11)
   cusolverDnHandle_t sol = nullptr;
   double *dense = nullptr, *dwork = nullptr;
@@ -266,15 +329,22 @@ struct lpfem_ctx {
 namespace {
 
 void setup_multi(lpfem_ctx* c);
-void halo_exchange(lpfem_ctx* c);
+RegionGrid region_grid(const lpfem_ctx* c, int reg);
 
 // ------------------------------------------------------------------------------------ host setup
 void upload_tables() {
-  static bool done = false;
+  // __constant__ tables live per device: upload once per device of this process
+  static std::mutex mu;
+  static bool done_dev[256] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 256) throw Err(LPFEM_EINVAL, "device index");
+  bool& done = done_dev[dev];
   if (done) return;
   KuhnTables kt[4];
   for (int d = 1; d <= 3; ++d) build_kuhn(d, kt[d]);
-  CK(cudaMemcpyToSymbol(c_kt, kt, sizeof(kt)));
+  CK(cpysym(c_kt, kt, sizeof(kt)));
   // neighbour offsets per parity class, from the simplices around an interior reference node
   static signed char nb[4][8][72][3], nb1[4][8][32][3];
   static int nbn[4][8], nb1n[4][8];
@@ -327,10 +397,10 @@ void upload_tables() {
         for (int a = 0; a < 3; ++a) nb1[d][k][i][a] = (signed char)p1[i][a];
     }
   }
-  CK(cudaMemcpyToSymbol(c_nb, nb, sizeof(nb)));
-  CK(cudaMemcpyToSymbol(c_nbn, nbn, sizeof(nbn)));
-  CK(cudaMemcpyToSymbol(c_nb1, nb1, sizeof(nb1)));
-  CK(cudaMemcpyToSymbol(c_nb1n, nb1n, sizeof(nb1n)));
+  CK(cpysym(c_nb, nb, sizeof(nb)));
+  CK(cpysym(c_nbn, nbn, sizeof(nbn)));
+  CK(cpysym(c_nb1, nb1, sizeof(nb1)));
+  CK(cpysym(c_nb1n, nb1n, sizeof(nb1n)));
   done = true;
 }
 
@@ -371,7 +441,7 @@ void build_pattern(lpfem_ctx* c, Family& F) {
   cudaStream_t st = c->st;
   const int nsys = (int)F.hs.size();
   F.ds = dalloc<SysDesc>(nsys);
-  CK(cudaMemcpyAsync(F.ds, F.hs.data(), nsys * sizeof(SysDesc), cudaMemcpyHostToDevice, st));
+  CK(cpya(F.ds, F.hs.data(), nsys * sizeof(SysDesc), cudaMemcpyHostToDevice, st));
   long long* cnt = dalloc<long long>(F.rows + 1);
   CK(cudaMemsetAsync(cnt, 0, (F.rows + 1) * sizeof(long long), st));
   k_pattern_count<D><<<grid_rows(F.maxrows, nsys), 128, 0, st>>>(F.ds, F.kind, cnt);
@@ -381,18 +451,55 @@ void build_pattern(lpfem_ctx* c, Family& F) {
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, F.rowptr, F.rows + 1, st));
   void* dtmp = dalloc<char>(tmp);
   CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, cnt, F.rowptr, F.rows + 1, st));
-  CK(cudaMemcpyAsync(&F.nnz, F.rowptr + F.rows, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cpya(&F.nnz, F.rowptr + F.rows, sizeof(long long), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   cudaFree(dtmp);
   cudaFree(cnt);
   {
     std::vector<long long> rp(F.rows + 1);
-    CK(cudaMemcpy(rp.data(), F.rowptr, (F.rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
+    CK(cpy(rp.data(), F.rowptr, (F.rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost));
     for (auto& S : F.hs) F.sys_nnz.push_back(rp[S.row_off + S.nrows] - rp[S.row_off]);
     F.hrp = std::move(rp);
   }
   F.col = dalloc<int>(F.nnz);
   k_pattern_fill<D><<<grid_rows(F.maxrows, nsys), 128, 0, st>>>(F.ds, F.kind, F.rowptr, F.col);
+  CKL();
+}
+
+// node-blocked copy of a conduit family's operator (krylov.cuh NBMat): lengths, pointers and columns (once)
+template <int D>
+void build_nb(lpfem_ctx* c, Family& F) {
+  cudaStream_t st = c->st;
+  const int ns = (int)F.hs.size();
+  const long long ni = F.nb_items;
+  F.nbioff = dalloc<long long>(ns);
+  CK(cpy(F.nbioff, F.h_ioff.data(), ns * sizeof(long long), cudaMemcpyHostToDevice));
+  F.nblen = dalloc<int2>(ni);
+  long long* cc = dalloc<long long>(ni + 1);
+  long long* vc = dalloc<long long>(ni + 1);
+  CK(cudaMemsetAsync(cc, 0, (ni + 1) * sizeof(long long), st));
+  CK(cudaMemsetAsync(vc, 0, (ni + 1) * sizeof(long long), st));
+  k_nb_len<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, F.nbioff, F.rowptr, F.col, F.nblen, cc, vc);
+  CKL();
+  F.nbcptr = dalloc<long long>(ni + 1);
+  F.nbvptr = dalloc<long long>(ni + 1);
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cc, F.nbcptr, ni + 1, st));
+  void* dtmp = dalloc<char>(tmp);
+  CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, cc, F.nbcptr, ni + 1, st));
+  CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, vc, F.nbvptr, ni + 1, st));
+  long long tot[2];
+  CK(cpya(&tot[0], F.nbcptr + ni, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cpya(&tot[1], F.nbvptr + ni, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dtmp);
+  cudaFree(cc);
+  cudaFree(vc);
+  if (tot[1] != F.nnz) throw Err(LPFEM_ESTATE, "node-blocked operator: value count differs from the CSR");
+  F.nb_ncols = tot[0];
+  F.nbcol = dalloc<int>(F.nb_ncols);
+  F.nbval = dalloc<double>(F.nnz);
+  k_nb_cols<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, F.nbioff, F.rowptr, F.col, F.nblen, F.nbcptr, F.nbcol);
   CKL();
 }
 
@@ -430,7 +537,9 @@ void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
   if (level_family) return;
   if (F.level == 1 && c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN) {
     F.ecorr = dalloc<double>(nv);
+    F.ecorr2 = dalloc<double>(nv);
     CK(cudaMemsetAsync(F.ecorr, 0, nv * sizeof(double), c->st));
+    CK(cudaMemsetAsync(F.ecorr2, 0, nv * sizeof(double), c->st));
   }
   // Krylov system list
   const int nsub = (int)F.hs.size();
@@ -445,17 +554,24 @@ void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
         F.hk.push_back(k);
       }
   } else {
+    long long io = 0;
     for (int s = 0; s < nsub; ++s) {
       KSys k{};
       k.row_off = F.hs[s].row_off;
       k.prow_off = F.hs[s].row_off;
       k.val_off = 0;
       k.nrows = F.hs[s].nrows;
+      k.item_off = io;
+      k.n2 = F.hs[s].n2;
+      k.n1 = F.hs[s].n1;
+      F.h_ioff.push_back(io);
+      io += F.hs[s].n2 + F.hs[s].n1;
       F.hk.push_back(k);
     }
+    F.nb_items = io;
   }
   F.dk = dalloc<KSys>(F.hk.size());
-  CK(cudaMemcpyAsync(F.dk, F.hk.data(), F.hk.size() * sizeof(KSys), cudaMemcpyHostToDevice, c->st));
+  CK(cpya(F.dk, F.hk.data(), F.hk.size() * sizeof(KSys), cudaMemcpyHostToDevice, c->st));
   F.dstat = dalloc<KStat>(F.hk.size());
   F.hstat.resize(F.hk.size());
 }
@@ -753,6 +869,11 @@ ConduitCoefs conduit_coefs(const lpfem_ctx* c, double dt, double hmin) {
 }
 
 template <int D>
+const ConvT<D>* convtp(const lpfem_ctx* c) {
+  return static_cast<const ConvT<D>*>(c->convt);
+}
+
+template <int D>
 const RefT<D>* refp(const lpfem_ctx* c) {
   return (const RefT<D>*)c->ref;
 }
@@ -875,16 +996,17 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.q = P.q;
   a.rows_total = 3 * P.rows;
   a.rtol = c->opts.krylov_rtol;
-  a.maxit = c->opts.max_iter;
+  a.maxit = (P.level == 1 && c->fault_maxit[0] > 0) ? c->fault_maxit[0] : c->opts.max_iter;
   a.stat = P.dstat;
   // warm start from the previous step's corrections (fine ML-PCG): measured fewer iterations, same test (C19)
   a.warm = (P.level == 1 && c->nlp > 0 && !c->kn.cold_start) ? std::min(P.solved, c->warm_order) : 0;
   a.xp = a.warm > 0 ? P.xp : nullptr;
+  a.order = P.level == 1 ? P.dorder : nullptr;
   P.solved = std::min(P.solved + 1, 2);
   const int ns = (int)P.hk.size();
   auto go_ml = [&](auto k) {
     if (!P.cluster_checked && !P.bandwidth_bound) {
-      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern), c->kn.verbose);
+      P.cluster = resident_cluster(k, P.nsys_rule, P.cluster, 1024, pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern), c->kn.verbose);
       P.cluster_checked = true;
     }
     const size_t sm = pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern);
@@ -893,7 +1015,7 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   };
   auto go = [&](auto k) {
     if (!P.cluster_checked && !P.bandwidth_bound) {
-      P.cluster = resident_cluster(k, ns, P.cluster, 1024, pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern), c->kn.verbose);
+      P.cluster = resident_cluster(k, P.nsys_rule, P.cluster, 1024, pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern), c->kn.verbose);
       P.cluster_checked = true;
     }
     const size_t sm = pattern_smem(k, P, P.cluster, 0, c->kn.no_smem_pattern);
@@ -926,11 +1048,15 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.V = C.V;
   a.rows_total = C.rows;
   a.rtol = c->opts.krylov_rtol;
-  a.maxit = c->opts.max_iter;
+  a.maxit = (C.level == 1 && c->fault_maxit[1] > 0) ? c->fault_maxit[1] : c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
   a.warm = (C.level == 1 && !c->kn.cold_start) ? std::min(C.solved, c->warm_order) : 0;
   a.xp = a.warm > 0 ? C.xp : nullptr;
+  a.order = C.level == 1 ? C.dorder : nullptr;
+  if (C.nbval) {
+    a.nb = NBMat{C.nbval, C.nbcol, C.nbvptr, C.nbcptr, C.nblen};
+  }
   C.solved = std::min(C.solved + 1, 2);
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
   // threshold reorthogonalised almost every iteration for identical iteration counts (cfg1-3), +20% GMRES time
@@ -948,10 +1074,10 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   const size_t hb = gmres_h_bytes(GM);
   auto go = [&](auto k) {
     if (!C.cluster_checked && !C.bandwidth_bound) {
-      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern), c->kn.verbose);
+      C.cluster = resident_cluster(k, C.nsys_rule, C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern || C.nbval), c->kn.verbose);
       C.cluster_checked = true;
     }
-    const size_t sm = pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern);
+    const size_t sm = pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern || C.nbval);
     a.smem_cols = sm > 0;
     launch_cluster_sm(k, (int)C.hk.size(), C.cluster, NTG, hb + sm, c->st, a, c->ml);
   };
@@ -970,8 +1096,8 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   if (C.level == 1) {
     std::vector<long long> h(16 * nsys_ph);
     std::vector<KStat> ks(nsys_ph);
-    CK(cudaMemcpyAsync(h.data(), ph, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(ks.data(), C.dstat, ks.size() * sizeof(KStat), cudaMemcpyDeviceToHost, c->st));
+    CK(cpya(h.data(), ph, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+    CK(cpya(ks.data(), C.dstat, ks.size() * sizeof(KStat), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     int worst = 0;
     for (int i = 0; i < nsys_ph; ++i)
@@ -1002,7 +1128,7 @@ void decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
   if (!C.hk.empty() && !C.cluster_checked && !C.bandwidth_bound) {
     const size_t hb = gmres_h_bytes(GM);
     auto chk = [&](auto k) {
-      C.cluster = resident_cluster(k, (int)C.hk.size(), C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern), c->kn.verbose);
+      C.cluster = resident_cluster(k, C.nsys_rule, C.cluster, NTG, hb + pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern || C.nbval), c->kn.verbose);
       C.cluster_checked = true;
     };
     const bool pc = c->nl > 0;
@@ -1016,14 +1142,32 @@ void decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
   }
   if (concurrent && !P.hk.empty() && !P.cluster_checked && !P.bandwidth_bound && !C.hk.empty() &&
       !C.bandwidth_bound) {
-    const int left = c->nsm - (int)C.hk.size() * C.cluster;
-    P.cluster = std::max(1, std::min(P.cluster, left / (int)P.hk.size()));
+    const int left = c->nsm - C.nsys_rule * C.cluster;
+    P.cluster = std::max(1, std::min(P.cluster, left / P.nsys_rule));
   }
+}
+
+// LPT launch order of a fine Krylov family: expected work rows x (iterations of the last solve + 1), largest first,
+// ties by index (deterministic); uploaded only when it changes.  Scheduling only: every system's arithmetic is the
+// same in any order.
+void set_order(lpfem_ctx* c, Family& F, bool from_stats) {
+  const int n = (int)F.hk.size();
+  if (n <= 1 || getenv("LPFEM_NO_ORDER")) return;
+  std::vector<double> w(n);
+  for (int i = 0; i < n; ++i) w[i] = (double)F.hk[i].nrows * (from_stats ? F.hstat[i].iters + 1.0 : 1.0);
+  std::vector<int> o(n);
+  for (int i = 0; i < n; ++i) o[i] = i;
+  std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return w[a] > w[b]; });
+  if (o == F.order) return;
+  F.order = o;
+  if (!F.dorder) F.dorder = dalloc<int>(n);
+  CK(cpya(F.dorder, F.order.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));  // F.order may change before the copy would run
 }
 
 void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres, bool& ok) {
   if (F.hk.empty()) return;
-  CK(cudaMemcpyAsync(F.hstat.data(), F.dstat, F.hstat.size() * sizeof(KStat), cudaMemcpyDeviceToHost, c->st));
+  CK(cpya(F.hstat.data(), F.dstat, F.hstat.size() * sizeof(KStat), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   long long mx = 0, sum = 0;
   for (auto& s : F.hstat) {
@@ -1037,19 +1181,27 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
   } else {
     c->stats.fine_iters[kind] += sum;
     c->stats.fine_max_iters[kind] = mx;
-    // algorithmic bytes: SpMV 12 B/nnz + 32 B/row per pass; CG vector work
-    // 64 B/row per iteration; GMRES 48 B/row per iteration + 16 B/row per basis vector per Gram-Schmidt.
+    // algorithmic bytes: SpMV 12 B/nnz + 32 B/row per pass (node-blocked conduit operator:
+    // 8 B/nnz + 4 B per (item, neighbour) column + 24 B per item + 16 B/row); CG vector work 64 B/row per
+    // iteration; GMRES 48 B/row per iteration + 16 B/row per basis vector per Gram-Schmidt.
     const int nsub = (int)F.hs.size();
     double bytes = 0.0;
     for (size_t i = 0; i < F.hstat.size(); ++i) {
       const int s = (int)(i % nsub);
       const double rows = F.hk[i].nrows, nz = (double)F.sys_nnz[s];
       const KStat& k = F.hstat[i];
-      bytes += k.spmv * (12.0 * nz + 32.0 * rows);
+      if (F.nbval) {
+        const double items = F.hk[i].n2 + F.hk[i].n1;
+        const double ncol = (double)F.nb_ncols * (nz / (double)F.nnz);  // the system's share of the columns
+        bytes += k.spmv * (8.0 * nz + 4.0 * ncol + 24.0 * items + 16.0 * rows);
+      } else {
+        bytes += k.spmv * (12.0 * nz + 32.0 * rows);
+      }
       bytes += kind == 0 ? 64.0 * rows * k.iters : 48.0 * rows * k.iters + 16.0 * rows * k.vsum;
     }
     c->stats.bytes_krylov[kind] += bytes;
     c->stats.krylov_launches[kind] += 1;
+    set_order(c, F, true);
   }
 }
 
@@ -1090,7 +1242,7 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
   solve_porous<D>(c, P);
   if (lev == 1) CK(cudaEventRecord(c->ek[1], st));
   k_porous_writeback<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(
-      P.ds, c->Lp[lev], P.z, P.x, P.isq, P.base, P.ecorr, out[0], out[1], out[2], 2 * c->Lp[lev].G.n[0] + 1,
+      P.ds, c->Lp[lev], P.z, P.x, P.isq, P.base, P.ecorr2, out[0], out[1], out[2], 2 * c->Lp[lev].G.n[0] + 1,
       2 * c->Lp[lev].G.n[1] + 1, 2 * c->Lp[lev].G.n[2] + 1, P.rows);
   CKL();
 }
@@ -1120,9 +1272,10 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
   double hmin = 1e300;
   for (int a = 0; a < D; ++a) hmin = std::min(hmin, L.G.hc[a]);
   const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
-  k_conduit_step<D><<<grid_rows(F.maxrows, ns, 256), 256, 0, st>>>(F.ds, L, cc, 1, c->kmult, c->nc_p[0], c->nc_p[1],
-                                                               c->nc_p[2], refp<D>(c), F.rowptr, F.col, F.aconst,
-                                                               F.mask, F.z, F.W, F.lag, F.qf, F.aux, F.aout, F.rhs);
+  k_conduit_step_nb<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, L, cc, 1, c->kmult, c->nc_p[0], c->nc_p[1],
+                                                                c->nc_p[2], refp<D>(c), convtp<D>(c), F.rowptr, F.col,
+                                                                F.aconst, F.mask, F.z, F.W, F.lag, F.qf, F.aux, F.aout,
+                                                                F.rhs);
   CKL();
   const long long tot = c->haoff.back();
   CK(cudaMemsetAsync(c->abuf, 0, tot * sizeof(double), st));
@@ -1138,17 +1291,27 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
     CKL();
     cm = c->abuf;
   } else {
-    // large boxes (3D): dense LU per matrix (cuSOLVER), inverse by solving with the identity
+    // large boxes (3D): dense LU per matrix (cuSOLVER), inverse by solving with the identity; the boxes are
+    // spread round robin over nsi streams with their own handles and workspaces (one box's LU does not fill the
+    // GPU: n = 1.1k-2.3k at cfg4)
     k_set_identity<<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, c->daoff, c->aci);
     CKL();
+    CK(cudaEventRecord(c->einv[c->nsi], st));
+    for (int k = 0; k < c->nsi; ++k) CK(cudaStreamWaitEvent(c->sinv[k], c->einv[c->nsi], 0));
     for (int s2 = 0; s2 < ns; ++s2) {
+      const int k = s2 % c->nsi;
       const int n = F.hs[s2].nrows;
       double* As = c->abuf + c->haoff[s2];
       double* Bs = c->aci + c->haoff[s2];
-      if (cusolverDnDgetrf(c->sol2, n, n, As, n, c->lwk2, c->lpiv2, c->linfo2) != CUSOLVER_STATUS_SUCCESS)
+      if (cusolverDnDgetrf(c->hinv[k], n, n, As, n, c->lwki[k], c->lpivi[k], c->linfoi[k]) != CUSOLVER_STATUS_SUCCESS)
         throw Err(LPFEM_ECUDA, "cusolverDnDgetrf (coarse box)");
-      if (cusolverDnDgetrs(c->sol2, CUBLAS_OP_N, n, n, As, n, c->lpiv2, Bs, n, c->linfo2) != CUSOLVER_STATUS_SUCCESS)
+      if (cusolverDnDgetrs(c->hinv[k], CUBLAS_OP_N, n, n, As, n, c->lpivi[k], Bs, n, c->linfoi[k]) !=
+          CUSOLVER_STATUS_SUCCESS)
         throw Err(LPFEM_ECUDA, "cusolverDnDgetrs (coarse box)");
+    }
+    for (int k = 0; k < c->nsi; ++k) {
+      CK(cudaEventRecord(c->einv[k], c->sinv[k]));
+      CK(cudaStreamWaitEvent(st, c->einv[k], 0));
     }
   }
   k_inv_rowmajor<float><<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, cm, c->ainv[slot]);
@@ -1193,11 +1356,14 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   }
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
-  k_conduit_step<D><<<grid_rows(C.maxrows, ns, 256), 256, 0, st>>>(C.ds, c->Lc[lev], cc, newton, c->kmult,
-                                                               c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), C.rowptr,
-                                                               C.col, C.aconst, colscale, C.z, C.W, C.lag, C.qf, C.aux,
-                                                               C.aout, C.rhs);
+  k_conduit_step_nb<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(
+      C.ds, c->Lc[lev], cc, newton, c->kmult, c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), convtp<D>(c), C.rowptr,
+      C.col, C.aconst, colscale, C.z, C.W, C.lag, C.qf, C.aux, C.aout, C.rhs);
   CKL();
+  if (C.nbval) {
+    k_nb_pack<D><<<grid_rows(C.maxitems * 32, ns), 128, 0, st>>>(C.ds, C.nbioff, C.rowptr, C.aout, C.nbvptr, C.nbval);
+    CKL();
+  }
   if (lev == 0) {
     // The system is in correction form around the current iterate z (rhs = b(W) - J(W) z, the nonlinear
     // residual), so any nonsingular matrix gives a convergent fixed-point map near the solution when it is
@@ -1217,14 +1383,14 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
       c->clu_dt = c->cur_dt;
       c->stats.coarse_factorizations++;
     }
-    CK(cudaMemcpyAsync(C.x, C.rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(cpya(C.x, C.rhs, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
     if (cusolverDnDgetrs(c->sol2, CUBLAS_OP_N, n, 1, c->dense, n, c->piv, C.x, n, c->dinfo) != CUSOLVER_STATUS_SUCCESS)
       throw Err(LPFEM_ECUDA, "cusolverDnDgetrs");
     KStat ks{};
     ks.iters = 1;
     ks.converged = 1;
     ks.spmv = 1;
-    CK(cudaMemcpyAsync(C.dstat, &ks, sizeof(KStat), cudaMemcpyHostToDevice, st));
+    CK(cpya(C.dstat, &ks, sizeof(KStat), cudaMemcpyHostToDevice, st));
   } else {
     if (lev == 1 && c->gate) CK(cudaEventRecord(c->evp[2], st));
     if (lev == 1) CK(cudaEventRecord(c->ek[2], st));
@@ -1233,7 +1399,7 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   }
   const int* npg = A.np_glob;
   k_conduit_writeback<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(C.ds, c->Lc[lev], C.z, C.x, colscale, C.base,
-                                                                    C.ecorr, out_u, out_p, npg[0], npg[1], npg[2],
+                                                                    C.ecorr2, out_u, out_p, npg[0], npg[1], npg[2],
                                                                     A.n2_glob);
   CKL();
 }
@@ -1245,13 +1411,30 @@ struct StreamSwap {  // route the launches of the shared stage functions to anot
   ~StreamSwap() { c->st = old; }
 };
 
+// C18: t_{n1} = t_base + (n1 - n_base) dt -- the product form (n1) dt while dt never changed (t_base = 0,
+// n_base = 0), and within every later constant-dt segment
+double time_at(const lpfem_ctx* c, long long n1, double dt) { return c->t_base + (double)(n1 - c->n_base) * dt; }
+
+// restores the coarse Navier-Stokes solver state when coarse_step leaves, normally or by an exception
+struct CoarseGuard {
+  lpfem_ctx* c;
+  int newton0;
+  int nexc;
+  explicit CoarseGuard(lpfem_ctx* cc) : c(cc), newton0(cc->coarse_newton), nexc(std::uncaught_exceptions()) {}
+  ~CoarseGuard() {
+    c->coarse_newton = newton0;
+    if (std::uncaught_exceptions() > nexc) c->clu_valid = false;  // the chord LU may be half-built
+  }
+};
+
 // Step 1: coarse state n -> n+1 (ring slots n % 3 -> (n+1) % 3), Algorithm 1 on T_H, on st2.
 template <int D>
 void coarse_step(lpfem_ctx* c, long long n, double dt) {
   StreamSwap sw(c, c->st2);
+  CoarseGuard guard(c);
   cudaStream_t st = c->st2;
   const int so = (int)(n % 3), sn = (int)((n + 1) % 3);
-  const double t = (double)(n + 1) * dt;  // C18
+  const double t = time_at(c, n + 1, dt);  // C18
   bool ok = true;
   CK(cudaEventRecord(c->evc[0], st));
   porous_stage<D>(c, 0, t, c->cst[so], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->cst[sn]);
@@ -1259,13 +1442,14 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
     double dummy = 0;
     fetch_stats(c, c->fam[0][0], 0, true, dummy, ok);
   }
+  CK(cudaEventRecord(c->evcp[0], st));
   const long long nu = (long long)D * c->n2c_c;
   bool pic_ok = false;
-  const int newton0 = c->coarse_newton;
+  const int newton0 = guard.newton0;
   for (int attempt = 0; attempt < 2 && !pic_ok; ++attempt) {
   if (attempt == 1) c->coarse_newton = 0;  // Newton failed: fall back to Picard from u^n
-  CK(cudaMemcpyAsync(c->wpic, c->cu[so], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(c->ppic, c->cp[so], c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cpya(c->wpic, c->cu[so], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cpya(c->ppic, c->cp[so], c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
   double du_prev = 0.0;
   if (attempt == 1) c->clu_force = true;
   for (int it = 0; it < c->opts.picard_max; ++it) {
@@ -1275,7 +1459,7 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
     k_picard_norms<<<1, 1024, 0, st>>>(c->wpic2, c->wpic, nu, c->nrm);
     CKL();
     double hn[2];
-    CK(cudaMemcpyAsync(hn, c->nrm, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cpya(hn, c->nrm, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     std::swap(c->wpic, c->wpic2);
     std::swap(c->ppic, c->ppic2);
@@ -1302,8 +1486,9 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
              " res " + std::to_string(st0.relres) + "]";
     throw Err(LPFEM_ENOCONV, m);
   }
-  CK(cudaMemcpyAsync(c->cu[sn], c->wpic, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(c->cp[sn], c->ppic, c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cpya(c->cu[sn], c->wpic, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cpya(c->cp[sn], c->ppic, c->n1c_c * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(c->evcp[1], st));
   // coarse-box inverses of the multilevel preconditioner for fine step n (Newton-linearised at U = P u_H^{n+1};
   // 3D reuses them for ml_refresh steps), into the slot the in-flight fine step does not read
   if (c->nl > 0 && !c->fam[1][1].hs.empty() &&
@@ -1316,28 +1501,49 @@ void coarse_step(lpfem_ctx* c, long long n, double dt) {
   }
   CK(cudaEventRecord(c->evc[1], st));
   CK(cudaEventSynchronize(c->evc[1]));
-  float ms = 0;
+  float ms = 0, m0 = 0, m1 = 0, m2 = 0;
   CK(cudaEventElapsedTime(&ms, c->evc[0], c->evc[1]));
+  CK(cudaEventElapsedTime(&m0, c->evc[0], c->evcp[0]));
+  CK(cudaEventElapsedTime(&m1, c->evcp[0], c->evcp[1]));
+  CK(cudaEventElapsedTime(&m2, c->evcp[1], c->evc[1]));
   c->stats.t_coarse_ms += ms;
+  c->stats.t_coarse_part_ms[0] += m0;
+  c->stats.t_coarse_part_ms[1] += m1;
+  c->stats.t_coarse_part_ms[2] += m2;
   c->coarse_n = n + 1;
   c->coarse_dt = dt;
 }
 
+// ---------------------------------------------------------------------------------------------- the step
+// lpfem_step = step_begin (coarse n+1 if not ready, fine corrections, write-back into the shadow composite,
+// halo pack) -> step_exchange (halo transfer + unpack into the shadow composite) -> step_overlap (coarse n+2
+// on the side stream) -> step_verdict (per-rank convergence) -> [reduction over the ranks] -> step_end
+// (commit = swap the shadow arrays in, or leave the state at t_n).  lpfem_step_group runs each phase for all
+// the contexts of a local group before the next phase.
+
+void halo_pack(lpfem_ctx* c);
+void halo_exchange_nccl(lpfem_ctx* c);
+void halo_unpack(lpfem_ctx* c);
+
 template <int D>
-void do_step(lpfem_ctx* c, double dt) {
+void step_begin(lpfem_ctx* c, double dt) {
+  CK(cudaSetDevice(c->dist.device));
   if (dt != c->cur_dt) {
     CK(cudaStreamSynchronize(c->st2));
     assemble_dt<D>(c, dt);  // on st; the coarse stream must see the new operators
     CK(cudaEventRecord(c->ev[3], c->st));
     CK(cudaStreamWaitEvent(c->st2, c->ev[3], 0));
     c->coarse_n = -1;  // a precomputed coarse step used the old dt
+    c->t_base = c->t_now;  // C18: the new dt takes effect at the committed state t_n
+    c->n_base = c->nstep;
   }
   cudaStream_t st = c->st;
   const long long n = c->nstep;
-  const double t = (double)(n + 1) * dt;  // C18
-  double maxres[2] = {0, 0};
-  bool ok = true;
-  // ---------------- Step 1: coarse state n+1 (precomputed during the previous step when dt is unchanged)
+  const double t = time_at(c, n + 1, dt);  // C18
+  c->pending_ok = true;
+  c->pending_t = t;
+  // ---------------- Step 1: coarse state n+1 (precomputed during the previous step when dt is unchanged; a
+  // precomputed step that did not converge left coarse_n behind, so it is recomputed -- and reported -- here)
   if (c->coarse_n != n + 1 || c->coarse_dt != dt) {
     c->coarse_n = n;
     coarse_step<D>(c, n, dt);
@@ -1345,7 +1551,7 @@ void do_step(lpfem_ctx* c, double dt) {
   CK(cudaEventRecord(c->evc[2], c->st2));
   CK(cudaStreamWaitEvent(st, c->evc[2], 0));
   const int so = (int)(n % 3), sn = (int)((n + 1) % 3);
-  // ---------------- Steps 3-4: fine corrections + write-back
+  // ---------------- Steps 3-4: fine corrections + write-back into the shadow composite comp2
   CK(cudaEventRecord(c->ev[1], st));
   // the porous and conduit corrections of a step are independent (each reads only coarse data and its own
   // region's lagged composite): the porous stage runs on st3 beside the conduit stage, its PCG gated behind the
@@ -1360,57 +1566,103 @@ void do_step(lpfem_ctx* c, double dt) {
     // identically (the local problems' right-hand sides are the residuals of the converged coarse step in the
     // same space): the composite is the coarse state n+1 (same mesh, same layout)
     for (int f = 0; f < 3; ++f)
-      CK(cudaMemcpyAsync(c->comp[f], c->cst[sn][f], c->n2p_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(c->comp_u, c->cu[sn], (size_t)D * c->n2c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(c->comp_p, c->cp[sn], c->n1c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CK(cpya(c->comp2[f], c->cst[sn][f], c->n2p_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(cpya(c->comp2_u, c->cu[sn], (size_t)D * c->n2c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(cpya(c->comp2_p, c->cp[sn], c->n1c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
   } else if (conc) {
     // conduit stage enqueued first (it records evp[2] just before its GMRES launch); the porous stage on st3
     // prepares concurrently and launches its PCG only after that point, on the SMs the GMRES leaves free
     CK(cudaEventRecord(c->evp[0], st));
     c->gate = true;
-    conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp_u, c->comp_p);
+    conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp2_u, c->comp2_p);
     CK(cudaStreamWaitEvent(c->st3, c->evp[0], 0));
     {
       StreamSwap sw(c, c->st3);
-      porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
+      porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp2);
     }
     c->gate = false;
     CK(cudaEventRecord(c->evp[1], c->st3));
     CK(cudaStreamWaitEvent(st, c->evp[1], 0));
   } else {
-    porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp);
-    conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp_u, c->comp_p);
+    porous_stage<D>(c, 1, t, c->cst[sn], c->cst[so], c->cu[so] + (D - 1) * c->n2c_c, c->comp2);
+    conduit_solve_once<D>(c, 1, t, c->cu[sn], c->cp[sn], c->cu[so], c->cst[so][2], c->comp2_u, c->comp2_p);
   }
-  halo_exchange(c);  // a11: refresh the overlaps of the lagged fields (C2 mode B), world > 1 only
-  CK(cudaEventRecord(c->ev[2], st));
-  // ---------------- Step 1 of the next step, overlapped with this fine stage (reads slot n+1, writes n+2)
+  halo_pack(c);  // a11 (world > 1): the owned values every peer reads, out of the new composite
+}
+
+// a11 transfer for the NCCL transport (the local transport's transfer is done by lpfem_step_group), then unpack
+void step_exchange(lpfem_ctx* c) {
+  if (c->dist.world <= 1) return;
+  if (c->dist.transport == LPFEM_TRANSPORT_NCCL) halo_exchange_nccl(c);
+  halo_unpack(c);
+}
+
+// Step 1 of the next step, overlapped with this fine stage (reads slot n+1, writes n+2).  A non-convergence there
+// is not this step's failure: coarse_n stays at n+1 and the next step recomputes (and reports) it.
+template <int D>
+void step_overlap(lpfem_ctx* c, double dt) {
+  CK(cudaEventRecord(c->ev[2], c->st));
   if (c->overlap && !c->kn.no_overlap) {
     try {
-      coarse_step<D>(c, n + 1, dt);
-    } catch (const Err&) {
-      c->coarse_n = n + 1;  // recomputed (and reported) at the next step
+      coarse_step<D>(c, c->nstep + 1, dt);
+    } catch (const Err& e) {
+      if (e.code != LPFEM_ENOCONV) throw;
+      c->coarse_n = c->nstep + 1;
     }
   }
+}
+
+// per-rank convergence of the step's fine solves (host sync)
+bool step_verdict(lpfem_ctx* c) {
+  const bool alg1 = c->R == 1 && !c->kn.no_alg1_fastpath;
+  double maxres[2] = {0, 0};
+  bool ok = true;
   if (!alg1) {
     fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
     fetch_stats(c, c->fam[1][1], 1, false, maxres[1], ok);
   } else {
-    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(c->st));
   }
+  c->pending_res[0] = maxres[0];
+  c->pending_res[1] = maxres[1];
+  c->pending_ok = ok;
+  return ok;
+}
+
+// NCCL: all ranks commit or none (min over the ranks' verdicts)
+bool reduce_verdict_nccl(lpfem_ctx* c, bool ok) {
+  if (c->dist.world <= 1 || c->dist.transport != LPFEM_TRANSPORT_NCCL) return ok;
+  int h = ok ? 1 : 0;
+  CK(cpya(c->dok, &h, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  CKN(g_nccl.allReduce(c->dok, c->dok, 1, ncclInt32, ncclMin, c->comm, c->st));
+  CK(cpya(&h, c->dok, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return h != 0;
+}
+
+void step_end(lpfem_ctx* c, bool ok_all) {
+  const bool alg1 = c->R == 1 && !c->kn.no_alg1_fastpath;
   float ms1 = 0, mk0 = 0, mk1 = 0;
   CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
   if (!alg1 && !c->fam[1][0].hs.empty()) CK(cudaEventElapsedTime(&mk0, c->ek[0], c->ek[1]));
   if (!alg1 && !c->fam[1][1].hs.empty()) CK(cudaEventElapsedTime(&mk1, c->ek[2], c->ek[3]));
   c->stats.t_krylov_ms[0] += mk0;
   c->stats.t_krylov_ms[1] += mk1;
-  c->stats.kernel_launches += tl_launches;
-  tl_launches = 0;
   c->stats.t_fine_ms += ms1;
-  c->stats.max_rel_residual[0] = maxres[0];
-  c->stats.max_rel_residual[1] = maxres[1];
+  c->stats.max_rel_residual[0] = c->pending_res[0];
+  c->stats.max_rel_residual[1] = c->pending_res[1];
+  if (!ok_all) {
+    if (!c->pending_ok) throw Err(LPFEM_ENOCONV, "a Krylov solve did not reach the relative residual (C19); step not committed");
+    throw Err(LPFEM_ENOCONV, "a Krylov solve of another rank did not converge (C19); step not committed");
+  }
+  // commit: the shadow arrays become the state at t_{n+1}
+  for (int f = 0; f < 3; ++f) std::swap(c->comp[f], c->comp2[f]);
+  std::swap(c->comp_u, c->comp2_u);
+  std::swap(c->comp_p, c->comp2_p);
+  for (int k = 0; k < 2; ++k) std::swap(c->fam[1][k].ecorr, c->fam[1][k].ecorr2);
+  c->t_now = c->pending_t;
   c->nstep++;
   c->stats.steps = c->nstep;
-  if (!ok) throw Err(LPFEM_ENOCONV, "a Krylov solve did not reach the relative residual (C19)");
 }
 
 template <int D>
@@ -1420,7 +1672,16 @@ void setup(lpfem_ctx* c) {
   RefT<D>* href = new RefT<D>();
   build_ref<D>(*href);
   c->ref = dalloc<RefT<D>>(1);
-  CK(cudaMemcpy(c->ref, href, sizeof(RefT<D>), cudaMemcpyHostToDevice));
+  CK(cpy(c->ref, href, sizeof(RefT<D>), cudaMemcpyHostToDevice));
+  {
+    KuhnTables kt;
+    build_kuhn(D, kt);
+    ConvT<D>* hct = new ConvT<D>();
+    build_convt<D>(*href, kt, *hct);
+    c->convt = dalloc<ConvT<D>>(1);
+    CK(cpy(c->convt, hct, sizeof(ConvT<D>), cudaMemcpyHostToDevice));
+    delete hct;
+  }
   delete href;
   const lpfem_geometry& g = c->geom;
   const double steps[2] = {c->H, c->h};
@@ -1468,9 +1729,10 @@ void setup(lpfem_ctx* c) {
   }
   // fine families: overlapping subdomains (Algorithm 3 Step 2; C7, C8)
   const int npos = c->m[0] * c->m[1] * (D > 2 ? c->m[2] : 1);
+  c->rank_of_pos = placement(region_grid(c, 0), region_grid(c, 1), c->dist.world);  // LPT (halo.h)
   std::vector<int> mine;
   for (int s = 0; s < npos; ++s)
-    if ((long long)s * c->dist.world / npos == c->dist.rank) mine.push_back(s);  // contiguous blocks
+    if (c->rank_of_pos[s] == c->dist.rank) mine.push_back(s);
   for (int k = 0; k < 2; ++k) {
     Family& F = c->fam[1][k];
     F.kind = k;
@@ -1521,6 +1783,9 @@ void setup(lpfem_ctx* c) {
       if (F.hs.empty()) continue;
       build_pattern<D>(c, F);
       alloc_vectors(c, F);
+      if (lev == 1) set_order(c, F, false);
+      // the fine conduit GMRES multiplies with a node-blocked copy of the operator (LPFEM_NO_NB: the CSR)
+      if (lev == 1 && k == 1 && !getenv("LPFEM_NO_NB")) build_nb<D>(c, F);
     }
   // multilevel preconditioner of the fine conduit systems: nested levels r h (r = 2, 4, .. dividing R)
   // and the coarse box at H (mlprec.cuh).  Requires the boxes to lie on coarse grid lines.
@@ -1595,7 +1860,7 @@ void setup(lpfem_ctx* c) {
           Stencil* hs0 = new Stencil();
           build_stencil<D>(r / rs[0], *hs0);
           Stencil* ds0 = dalloc<Stencil>(1);
-          CK(cudaMemcpy(ds0, hs0, sizeof(Stencil), cudaMemcpyHostToDevice));
+          CK(cpy(ds0, hs0, sizeof(Stencil), cudaMemcpyHostToDevice));
           delete hs0;
           c->stencils.push_back(ds0);
           c->ml.st0[l] = ds0;
@@ -1604,7 +1869,7 @@ void setup(lpfem_ctx* c) {
           Stencil* hst = new Stencil();
           build_stencil<D>(c->ml.direct == 1 ? r : c->ml.q[l], *hst);
           Stencil* dst = dalloc<Stencil>(1);
-          CK(cudaMemcpy(dst, hst, sizeof(Stencil), cudaMemcpyHostToDevice));
+          CK(cpy(dst, hst, sizeof(Stencil), cudaMemcpyHostToDevice));
           delete hst;
           c->stencils.push_back(dst);
           c->ml.st[l] = dst;
@@ -1631,8 +1896,8 @@ void setup(lpfem_ctx* c) {
       c->gjperm = dalloc<int>(atot);
       c->dpoff = dalloc<long long>(poff.size());
       c->daoff = dalloc<long long>(aoff.size());
-      CK(cudaMemcpy(c->dpoff, poff.data(), poff.size() * sizeof(long long), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(c->daoff, aoff.data(), aoff.size() * sizeof(long long), cudaMemcpyHostToDevice));
+      CK(cpy(c->dpoff, poff.data(), poff.size() * sizeof(long long), cudaMemcpyHostToDevice));
+      CK(cpy(c->daoff, aoff.data(), aoff.size() * sizeof(long long), cudaMemcpyHostToDevice));
       int nmax = 1;
       for (auto& S : c->lvl[c->nl - 1].hs) nmax = std::max(nmax, S.nrows);
       c->lpiv = dalloc<int>(nmax + 4096);
@@ -1711,10 +1976,10 @@ void setup(lpfem_ctx* c) {
           for (int f = 0; f < 3; ++f)
             for (auto& S3 : FL.hs) h3.push_back(S3);
           c->pds3 = dalloc<SysDesc>(h3.size());
-          CK(cudaMemcpy(c->pds3, h3.data(), h3.size() * sizeof(SysDesc), cudaMemcpyHostToDevice));
+          CK(cpy(c->pds3, h3.data(), h3.size() * sizeof(SysDesc), cudaMemcpyHostToDevice));
         }
         c->daoff_p = dalloc<long long>(aoffp.size());
-        CK(cudaMemcpy(c->daoff_p, aoffp.data(), aoffp.size() * sizeof(long long), cudaMemcpyHostToDevice));
+        CK(cpy(c->daoff_p, aoffp.data(), aoffp.size() * sizeof(long long), cudaMemcpyHostToDevice));
         FP.dinv = dalloc<double>(3 * FP.rows);
         FP.zv = dalloc<double>(3 * FP.rows);
         c->mlp.nl = c->nlp;
@@ -1728,16 +1993,21 @@ void setup(lpfem_ctx* c) {
       }
     }
   }
-  // cluster sizes: spread the systems of a family over the SMs (deterministic in the global layout)
+  // cluster sizes: spread the systems of a family over the SMs.  Default: from this rank's system counts.
+  // world_invariant: from the GLOBAL counts (the world-1 values), identical on every rank and every world size,
+  // so that every Krylov reduction has the same order for any world (bitwise world invariance)
   {
     int nsm = 148;
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, c->dist.device) == cudaSuccess) nsm = prop.multiProcessorCount;
     c->nsm = nsm;
+    const bool inv = c->opts.world_invariant != 0;
     for (int lev = 0; lev < 2; ++lev)
       for (int k = 0; k < 2; ++k) {
         Family& F = c->fam[lev][k];
-        const int nsys = std::max<int>(1, (int)F.hk.size());
+        const int nsys_loc = std::max<int>(1, (int)F.hk.size());
+        const int nsys = (inv && lev == 1) ? (k == 0 ? 3 : 1) * npos : nsys_loc;
+        F.nsys_rule = nsys;
         // one 1024-thread CTA per SM: start from nsm / nsys (<= 16, non-portable above 8); the first Krylov
         // launch lowers it until every cluster is resident at once (resident_cluster)
         int cl = std::max(1, std::min(16, nsm / nsys));
@@ -1747,7 +2017,8 @@ void setup(lpfem_ctx* c) {
         long long nzmax = 0;
         for (long long z : F.sys_nnz) nzmax = std::max(nzmax, z);
         const long long bw_nnz = getenv("LPFEM_BW_NNZ") ? atoll(getenv("LPFEM_BW_NNZ")) : 2000000;  // experiment
-        F.bandwidth_bound = nzmax > bw_nnz;
+        // world_invariant: a rule that does not depend on which boxes this rank holds (3D = bandwidth-bound)
+        F.bandwidth_bound = (inv && lev == 1) ? D == 3 : nzmax > bw_nnz;
         if (F.bandwidth_bound) {  // up to two waves: cfg4 cluster 2 / 4 / 8 -> GMRES 1865 / 1777 / 1833 ms
           cl = 1;
           while (cl < 16 && nsys * cl <= nsm) cl *= 2;
@@ -1768,12 +2039,17 @@ void setup(lpfem_ctx* c) {
   c->ppic = dalloc<double>(c->n1c_c);
   c->ppic2 = dalloc<double>(c->n1c_c);
   c->nrm = dalloc<double>(2);
-  for (int f = 0; f < 3; ++f) c->comp[f] = dalloc<double>(c->n2p_f);
+  for (int f = 0; f < 3; ++f) {
+    c->comp[f] = dalloc<double>(c->n2p_f);
+    c->comp2[f] = dalloc<double>(c->n2p_f);
+  }
   c->comp_u = dalloc<double>(D * c->n2c_f);
   c->comp_p = dalloc<double>(c->n1c_f);
+  c->comp2_u = dalloc<double>(D * c->n2c_f);
+  c->comp2_p = dalloc<double>(c->n1c_f);
   if (!c->hkmult.empty()) {
     c->kmult = dalloc<double>(c->hkmult.size());
-    CK(cudaMemcpy(c->kmult, c->hkmult.data(), c->hkmult.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cpy(c->kmult, c->hkmult.data(), c->hkmult.size() * sizeof(double), cudaMemcpyHostToDevice));
   }
   cudaStream_t st = c->st;
   // C12: u_H^0 = I_H u_0, u^h_0 = I_h u_0
@@ -1803,7 +2079,8 @@ void setup(lpfem_ctx* c) {
     {
       auto on = [](const char* k) { return getenv(k) != nullptr; };
       c->kn.verbose = on("LPFEM_VERBOSE");
-      c->kn.no_smem_pattern = on("LPFEM_NO_SMEM_PATTERN");
+      // world_invariant: the CTA shared-memory budget (hence the residency check) must not depend on the local boxes
+      c->kn.no_smem_pattern = on("LPFEM_NO_SMEM_PATTERN") || c->opts.world_invariant != 0;
       c->kn.cold_start = on("LPFEM_COLD_START");
       c->kn.coarse_full_newton = on("LPFEM_COARSE_FULL_NEWTON");
       c->kn.no_concurrent = on("LPFEM_NO_CONCURRENT");
@@ -1820,6 +2097,7 @@ void setup(lpfem_ctx* c) {
     c->ml_refresh = D == 2 ? 1 : 4;
     if (getenv("LPFEM_ML_REFRESH")) c->ml_refresh = std::max(1, atoi(getenv("LPFEM_ML_REFRESH")));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evc[i], cudaEventDefault));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->evcp[i], cudaEventDefault));
     if (cusolverDnCreate(&c->sol2) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
     cusolverDnSetStream(c->sol2, c->st2);
     c->dense = dalloc<double>((size_t)n * n);
@@ -1839,6 +2117,16 @@ void setup(lpfem_ctx* c) {
       c->lwk2 = dalloc<double>(std::max(1, c->llwork));
       c->lpiv2 = dalloc<int>(nmax + 4096);
       c->linfo2 = dalloc<int>(1);
+      c->nsi = nmax > c->kn.gj_max ? lpfem_ctx::NSI : 0;  // 3D boxes only (2D: batched Gauss-Jordan)
+      for (int k = 0; k < c->nsi; ++k) {
+        CK(cudaStreamCreateWithFlags(&c->sinv[k], cudaStreamNonBlocking));
+        if (cusolverDnCreate(&c->hinv[k]) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
+        cusolverDnSetStream(c->hinv[k], c->sinv[k]);
+        c->lwki[k] = dalloc<double>(std::max(1, c->llwork));
+        c->lpivi[k] = dalloc<int>(nmax + 4096);
+        c->linfoi[k] = dalloc<int>(1);
+      }
+      for (int k = 0; k <= c->nsi; ++k) CK(cudaEventCreateWithFlags(&c->einv[k], cudaEventDisableTiming));
     }
   }
   for (int i = 0; i < 4; ++i) {
@@ -1924,7 +2212,7 @@ __global__ void k_unpack(const int* __restrict__ idx, int n, double* f0, double*
 
 int* upload_ints(const std::vector<int>& v) {
   int* d = dalloc<int>(std::max<size_t>(1, v.size()));
-  if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (!v.empty()) CK(cpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
   return d;
 }
 
@@ -1939,15 +2227,51 @@ RegionGrid region_grid(const lpfem_ctx* c, int reg) {
   return G;
 }
 
+// ---- local transport: the contexts of one in-process group, by key (dist.nccl_id) and rank
+std::mutex g_groups_mu;
+std::map<std::string, std::vector<lpfem_ctx*>> g_groups;
+
+std::vector<lpfem_ctx*>& local_group(const lpfem_ctx* c) {
+  auto it = g_groups.find(c->group_key);
+  if (it == g_groups.end()) throw Err(LPFEM_ESTATE, "local group not registered");
+  return it->second;
+}
+
+lpfem_ctx* local_peer(const lpfem_ctx* c, int rank) {
+  std::vector<lpfem_ctx*>& g = local_group(c);
+  if (rank < 0 || rank >= (int)g.size() || !g[rank]) throw Err(LPFEM_ESTATE, "local group incomplete (rank " + std::to_string(rank) + ")");
+  return g[rank];
+}
+
+const PeerX& peer_entry(const lpfem_ctx* c, int peer) {
+  for (const PeerX& X : c->peers)
+    if (X.peer == peer) return X;
+  throw Err(LPFEM_ESTATE, "no peer entry");
+}
+
 void setup_multi(lpfem_ctx* c) {
-  if (!g_nccl.load()) throw Err(LPFEM_ENCCL, "cannot load libnccl.so.2");
-  ncclUniqueId id;
-  std::memcpy(&id, c->dist.nccl_id, sizeof(id));
-  CKN(g_nccl.commInitRank(&c->comm, c->dist.world, id, c->dist.rank));
   const int me = c->dist.rank, W = c->dist.world;
-  plan_region(region_grid(c, 0), me, W, false, c->plan_p);
-  plan_region(region_grid(c, 1), me, W, false, c->plan_c2);
-  plan_region(region_grid(c, 1), me, W, true, c->plan_c1);
+  if (c->dist.transport == LPFEM_TRANSPORT_NCCL) {
+    if (!g_nccl.load()) throw Err(LPFEM_ENCCL, "cannot load libnccl.so.2");
+    ncclUniqueId id;
+    std::memcpy(&id, c->dist.nccl_id, sizeof(id));
+    CKN(g_nccl.commInitRank(&c->comm, c->dist.world, id, c->dist.rank));
+    c->dok = dalloc<int>(1);
+  } else if (c->dist.transport == LPFEM_TRANSPORT_LOCAL) {
+    c->group_key.assign((const char*)c->dist.nccl_id, sizeof(c->dist.nccl_id));
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    std::vector<lpfem_ctx*>& g = g_groups[c->group_key];
+    if (g.empty()) g.assign(W, nullptr);
+    if ((int)g.size() != W || g[me]) throw Err(LPFEM_EINVAL, "local group: world or rank clash");
+    g[me] = c;
+    CK(cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_xdone, cudaEventDisableTiming));
+  } else {
+    throw Err(LPFEM_EINVAL, "unknown transport");
+  }
+  plan_region(region_grid(c, 0), c->rank_of_pos, me, W, false, c->plan_p);
+  plan_region(region_grid(c, 1), c->rank_of_pos, me, W, false, c->plan_c2);
+  plan_region(region_grid(c, 1), c->rank_of_pos, me, W, true, c->plan_c1);
   for (int p = 0; p < W; ++p) {
     if (p == me) continue;
     PeerX X;
@@ -1964,31 +2288,44 @@ void setup_multi(lpfem_ctx* c) {
     X.rbuf = dalloc<double>(3LL * X.np_need + (long long)c->D * X.nc_need + 1);
     c->peers.push_back(X);
   }
+  // owned lists of every rank (any rank may be the root of lpfem_get_fields): uploaded once, here
   long long mx = 1;
-  for (int p = 0; p < W; ++p)
+  for (int p = 0; p < W; ++p) {
+    c->own_p.push_back(upload_ints(c->plan_p.owned[p]));
+    c->own_c2.push_back(upload_ints(c->plan_c2.owned[p]));
+    c->own_c1.push_back(upload_ints(c->plan_c1.owned[p]));
     mx = std::max<long long>(mx, 3LL * c->plan_p.owned[p].size() + (long long)c->D * c->plan_c2.owned[p].size() +
                                      c->plan_c1.owned[p].size());
+  }
   c->gbuf_n = mx;
   c->gbuf = dalloc<double>(mx);
 }
 
-// overlap refresh after the write-back: owned values of the lagged fields to every peer that reads them
-void halo_exchange(lpfem_ctx* c) {
+// a11 after the write-back: the owned values of the lagged fields (3 porous P2 + d velocity P2, C2 mode B) that
+// each peer's extended boxes read, out of the new composite (comp2), into one send buffer per peer
+void halo_pack(lpfem_ctx* c) {
   if (c->dist.world <= 1) return;
   cudaStream_t st = c->st;
   const int D = c->D;
   const long long n2c = c->n2c_f;
   for (auto& X : c->peers) {
     if (X.np_give) {
-      k_pack<<<(X.np_give + 255) / 256, 256, 0, st>>>(X.give_p, X.np_give, c->comp[0], c->comp[1], c->comp[2], X.sbuf);
+      k_pack<<<(X.np_give + 255) / 256, 256, 0, st>>>(X.give_p, X.np_give, c->comp2[0], c->comp2[1], c->comp2[2], X.sbuf);
       CKL();
     }
     if (X.nc_give) {
-      k_pack<<<(X.nc_give + 255) / 256, 256, 0, st>>>(X.give_c, X.nc_give, c->comp_u, c->comp_u + n2c,
-                                                      D > 2 ? c->comp_u + 2 * n2c : nullptr, X.sbuf + 3LL * X.np_give);
+      k_pack<<<(X.nc_give + 255) / 256, 256, 0, st>>>(X.give_c, X.nc_give, c->comp2_u, c->comp2_u + n2c,
+                                                      D > 2 ? c->comp2_u + 2 * n2c : nullptr, X.sbuf + 3LL * X.np_give);
       CKL();
     }
   }
+  if (c->dist.transport == LPFEM_TRANSPORT_LOCAL) CK(cudaEventRecord(c->ev_pack, st));
+}
+
+// NCCL transport: one group of send/recv per peer pair
+void halo_exchange_nccl(lpfem_ctx* c) {
+  cudaStream_t st = c->st;
+  const int D = c->D;
   CKN(g_nccl.groupStart());
   for (auto& X : c->peers) {
     const size_t ns = 3ULL * X.np_give + (size_t)D * X.nc_give, nr = 3ULL * X.np_need + (size_t)D * X.nc_need;
@@ -1996,73 +2333,124 @@ void halo_exchange(lpfem_ctx* c) {
     if (nr) CKN(g_nccl.recv(X.rbuf, nr, ncclFloat64, X.peer, c->comm, st));
   }
   CKN(g_nccl.groupEnd());
+}
+
+// local transport: copy each peer's send buffer for this rank (packed by the peer's step_begin) into the receive
+// buffer, after the peer's pack event
+void halo_exchange_local(lpfem_ctx* c) {
+  cudaStream_t st = c->st;
+  const int D = c->D;
+  for (auto& X : c->peers) {
+    lpfem_ctx* q = local_peer(c, X.peer);
+    const PeerX& Y = peer_entry(q, c->dist.rank);
+    const size_t nr = 3ULL * X.np_need + (size_t)D * X.nc_need;
+    if (Y.np_give != X.np_need || Y.nc_give != X.nc_need) throw Err(LPFEM_ESTATE, "local halo: list sizes differ");
+    CK(cudaStreamWaitEvent(st, q->ev_pack, 0));
+    if (nr) CK(cudaMemcpyPeerAsync(X.rbuf, c->dist.device, Y.sbuf, q->dist.device, nr * sizeof(double), st));
+  }
+  CK(cudaEventRecord(c->ev_xdone, st));
+}
+
+void halo_unpack(lpfem_ctx* c) {
+  cudaStream_t st = c->st;
+  const int D = c->D;
+  const long long n2c = c->n2c_f;
   for (auto& X : c->peers) {
     if (X.np_need) {
-      k_unpack<<<(X.np_need + 255) / 256, 256, 0, st>>>(X.need_p, X.np_need, c->comp[0], c->comp[1], c->comp[2],
+      k_unpack<<<(X.np_need + 255) / 256, 256, 0, st>>>(X.need_p, X.np_need, c->comp2[0], c->comp2[1], c->comp2[2],
                                                         X.rbuf);
       CKL();
     }
     if (X.nc_need) {
-      k_unpack<<<(X.nc_need + 255) / 256, 256, 0, st>>>(X.need_c, X.nc_need, c->comp_u, c->comp_u + n2c,
-                                                        D > 2 ? c->comp_u + 2 * n2c : nullptr,
+      k_unpack<<<(X.nc_need + 255) / 256, 256, 0, st>>>(X.need_c, X.nc_need, c->comp2_u, c->comp2_u + n2c,
+                                                        D > 2 ? c->comp2_u + 2 * n2c : nullptr,
                                                         X.rbuf + 3LL * X.np_need);
       CKL();
     }
   }
 }
 
-// gather every rank's owned composite values on root (collective)
+// pack rank p's owned composite values (committed state) into buf
+void pack_owned(lpfem_ctx* q, int p, double* buf, cudaStream_t st) {
+  const int D = q->D;
+  const long long n2c = q->n2c_f;
+  const int np = (int)q->plan_p.owned[p].size(), nc2 = (int)q->plan_c2.owned[p].size(),
+            nc1 = (int)q->plan_c1.owned[p].size();
+  if (np) k_pack<<<(np + 255) / 256, 256, 0, st>>>(q->own_p[p], np, q->comp[0], q->comp[1], q->comp[2], buf);
+  if (nc2)
+    k_pack<<<(nc2 + 255) / 256, 256, 0, st>>>(q->own_c2[p], nc2, q->comp_u, q->comp_u + n2c,
+                                              D > 2 ? q->comp_u + 2 * n2c : nullptr, buf + 3LL * np);
+  if (nc1) k_pack<<<(nc1 + 255) / 256, 256, 0, st>>>(q->own_c1[p], nc1, q->comp_p, nullptr, nullptr,
+                                                     buf + 3LL * np + (long long)D * nc2);
+  CKL();
+}
+
+void unpack_owned(lpfem_ctx* c, int p, const double* buf, cudaStream_t st) {
+  const int D = c->D;
+  const long long n2c = c->n2c_f;
+  const int np = (int)c->plan_p.owned[p].size(), nc2 = (int)c->plan_c2.owned[p].size(),
+            nc1 = (int)c->plan_c1.owned[p].size();
+  if (np) k_unpack<<<(np + 255) / 256, 256, 0, st>>>(c->own_p[p], np, c->comp[0], c->comp[1], c->comp[2], buf);
+  if (nc2)
+    k_unpack<<<(nc2 + 255) / 256, 256, 0, st>>>(c->own_c2[p], nc2, c->comp_u, c->comp_u + n2c,
+                                                D > 2 ? c->comp_u + 2 * n2c : nullptr, buf + 3LL * np);
+  if (nc1) k_unpack<<<(nc1 + 255) / 256, 256, 0, st>>>(c->own_c1[p], nc1, c->comp_p, nullptr, nullptr,
+                                                       buf + 3LL * np + (long long)D * nc2);
+  CKL();
+}
+
+size_t owned_count(const lpfem_ctx* c, int p) {
+  return 3ULL * c->plan_p.owned[p].size() + (size_t)c->D * c->plan_c2.owned[p].size() + c->plan_c1.owned[p].size();
+}
+
+// gather every rank's owned composite values on root: NCCL send/recv (collective), or (local transport) the root
+// packs each peer's values on the peer's stream and copies them over
 void gather_root(lpfem_ctx* c, int root) {
   if (c->dist.world <= 1) return;
   cudaStream_t st = c->st;
-  const int D = c->D, me = c->dist.rank;
-  const long long n2c = c->n2c_f;
-  auto lists = [&](int p, int*& ip, int*& ic2, int*& ic1) {
-    ip = upload_ints(c->plan_p.owned[p]);
-    ic2 = upload_ints(c->plan_c2.owned[p]);
-    ic1 = upload_ints(c->plan_c1.owned[p]);
-  };
+  const int me = c->dist.rank;
+  if (c->dist.transport == LPFEM_TRANSPORT_LOCAL) {
+    if (me != root) return;
+    for (int p = 0; p < c->dist.world; ++p) {
+      if (p == root) continue;
+      lpfem_ctx* q = local_peer(c, p);
+      CK(cudaSetDevice(q->dist.device));
+      pack_owned(q, p, q->gbuf, q->st);
+      CK(cudaEventRecord(q->ev_pack, q->st));
+      CK(cudaSetDevice(c->dist.device));
+      CK(cudaStreamWaitEvent(st, q->ev_pack, 0));
+      CK(cudaMemcpyPeerAsync(c->gbuf, c->dist.device, q->gbuf, q->dist.device, owned_count(c, p) * sizeof(double), st));
+      unpack_owned(c, p, c->gbuf, st);
+      CK(cudaStreamSynchronize(st));  // gbuf is reused for the next peer
+    }
+    return;
+  }
   if (me != root) {
-    int *ip, *ic2, *ic1;
-    lists(me, ip, ic2, ic1);
-    const int np = (int)c->plan_p.owned[me].size(), nc2 = (int)c->plan_c2.owned[me].size(),
-              nc1 = (int)c->plan_c1.owned[me].size();
-    if (np) k_pack<<<(np + 255) / 256, 256, 0, st>>>(ip, np, c->comp[0], c->comp[1], c->comp[2], c->gbuf);
-    if (nc2)
-      k_pack<<<(nc2 + 255) / 256, 256, 0, st>>>(ic2, nc2, c->comp_u, c->comp_u + n2c,
-                                                D > 2 ? c->comp_u + 2 * n2c : nullptr, c->gbuf + 3LL * np);
-    if (nc1) k_pack<<<(nc1 + 255) / 256, 256, 0, st>>>(ic1, nc1, c->comp_p, nullptr, nullptr,
-                                                       c->gbuf + 3LL * np + (long long)D * nc2);
-    CKL();
-    const size_t n = 3ULL * np + (size_t)D * nc2 + nc1;
-    CKN(g_nccl.send(c->gbuf, n, ncclFloat64, root, c->comm, st));
+    pack_owned(c, me, c->gbuf, st);
+    CKN(g_nccl.send(c->gbuf, owned_count(c, me), ncclFloat64, root, c->comm, st));
     CK(cudaStreamSynchronize(st));
-    cudaFree(ip);
-    cudaFree(ic2);
-    cudaFree(ic1);
   } else {
     for (int p = 0; p < c->dist.world; ++p) {
       if (p == root) continue;
-      int *ip, *ic2, *ic1;
-      lists(p, ip, ic2, ic1);
-      const int np = (int)c->plan_p.owned[p].size(), nc2 = (int)c->plan_c2.owned[p].size(),
-                nc1 = (int)c->plan_c1.owned[p].size();
-      const size_t n = 3ULL * np + (size_t)D * nc2 + nc1;
-      CKN(g_nccl.recv(c->gbuf, n, ncclFloat64, p, c->comm, st));
-      if (np) k_unpack<<<(np + 255) / 256, 256, 0, st>>>(ip, np, c->comp[0], c->comp[1], c->comp[2], c->gbuf);
-      if (nc2)
-        k_unpack<<<(nc2 + 255) / 256, 256, 0, st>>>(ic2, nc2, c->comp_u, c->comp_u + n2c,
-                                                    D > 2 ? c->comp_u + 2 * n2c : nullptr, c->gbuf + 3LL * np);
-      if (nc1) k_unpack<<<(nc1 + 255) / 256, 256, 0, st>>>(ic1, nc1, c->comp_p, nullptr, nullptr,
-                                                           c->gbuf + 3LL * np + (long long)D * nc2);
-      CKL();
-      CK(cudaStreamSynchronize(st));
-      cudaFree(ip);
-      cudaFree(ic2);
-      cudaFree(ic1);
+      CKN(g_nccl.recv(c->gbuf, owned_count(c, p), ncclFloat64, p, c->comm, st));
+      unpack_owned(c, p, c->gbuf, st);
     }
+    CK(cudaStreamSynchronize(st));
   }
 }
+
+// adds this call's kernel launches and host<->device bytes (thread-local counters) to a ctx's statistics
+struct Counted {
+  lpfem_ctx* c;
+  long long l0, h0, d0;
+  explicit Counted(lpfem_ctx* cc) : c(cc), l0(tl_launches), h0(tl_h2d), d0(tl_d2h) {}
+  ~Counted() {
+    if (!c) return;
+    c->stats.kernel_launches += tl_launches - l0;
+    c->stats.h2d_bytes += tl_h2d - h0;
+    c->stats.d2h_bytes += tl_d2h - d0;
+  }
+};
 
 lpfem_status fail(lpfem_ctx* c, const Err& e) {
   if (c) c->err = e.what();
@@ -2147,7 +2535,9 @@ lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs
       c->dist.rank = 0;
       c->dist.world = 1;
       c->dist.device = 0;
+      c->dist.transport = LPFEM_TRANSPORT_NCCL;
     }
+    if (c->dist.world == 1) c->group_key.clear();
     if (c->dist.world < 1 || c->dist.rank < 0 || c->dist.rank >= c->dist.world) throw Err(LPFEM_EINVAL, "bad dist");
     CK(cudaSetDevice(c->dist.device));
     c->st = (cudaStream_t)c->dist.cuda_stream;
@@ -2157,7 +2547,10 @@ lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs
         ncells *= to_int_checked((geom->porous_hi[a] - geom->porous_lo[a]) / H, LPFEM_ENOTDIV, "porous extent / H");
       c->hkmult.assign(coeffs->k_mult, coeffs->k_mult + ncells);
     }
-    if (c->D == 2) setup<2>(c); else setup<3>(c);
+    {
+      Counted cnt(c);
+      if (c->D == 2) setup<2>(c); else setup<3>(c);
+    }
     *out = c;
     return LPFEM_OK;
   } catch (const Err& e) {
@@ -2174,12 +2567,84 @@ lpfem_status lpfem_step(lpfem_ctx* c, double dt) {
     c->err = "dt must be > 0";
     return LPFEM_EINVAL;
   }
+  if (c->dist.world > 1 && c->dist.transport == LPFEM_TRANSPORT_LOCAL) {
+    c->err = "local-transport contexts are stepped by lpfem_step_group";
+    return LPFEM_ESTATE;
+  }
+  Counted cnt(c);
   try {
-    if (c->D == 2) do_step<2>(c, dt); else do_step<3>(c, dt);
+    if (c->D == 2) step_begin<2>(c, dt); else step_begin<3>(c, dt);
+    step_exchange(c);
+    if (c->D == 2) step_overlap<2>(c, dt); else step_overlap<3>(c, dt);
+    const bool ok = reduce_verdict_nccl(c, step_verdict(c));
+    step_end(c, ok);
     return LPFEM_OK;
   } catch (const Err& e) {
     return fail(c, e);
   }
+}
+
+lpfem_status lpfem_step_group(lpfem_ctx* const* ctxs, int n, double dt) {
+  if (!ctxs || n < 1 || !(dt > 0)) return LPFEM_EINVAL;
+  // the contexts must be exactly the ranks of one local group
+  std::vector<lpfem_ctx*> g(n, nullptr);
+  for (int i = 0; i < n; ++i) {
+    lpfem_ctx* c = ctxs[i];
+    if (!c || c->dist.world != n || c->dist.rank < 0 || c->dist.rank >= n || g[c->dist.rank]) return LPFEM_EINVAL;
+    if (n > 1 && c->dist.transport != LPFEM_TRANSPORT_LOCAL) return LPFEM_EINVAL;
+    if (c->group_key != ctxs[0]->group_key) return LPFEM_EINVAL;
+    g[c->dist.rank] = c;
+  }
+  lpfem_ctx* cur = g[0];
+  Counted cnt(g[0]);  // the group's launches and copies are accounted on rank 0
+  try {
+    for (lpfem_ctx* c : g) {  // phase 1: coarse (if needed), fine stage, write-back, pack
+      cur = c;
+      if (c->D == 2) step_begin<2>(c, dt); else step_begin<3>(c, dt);
+    }
+    if (n > 1) {
+      for (lpfem_ctx* c : g) {  // phase 2: transfers (after every peer's pack) and unpack
+        cur = c;
+        CK(cudaSetDevice(c->dist.device));
+        halo_exchange_local(c);
+        halo_unpack(c);
+      }
+      // a peer's send buffers are rewritten by its next pack only after every copy out of them is done
+      for (lpfem_ctx* c : g) {
+        cur = c;
+        CK(cudaSetDevice(c->dist.device));
+        for (lpfem_ctx* q : g)
+          if (q != c) CK(cudaStreamWaitEvent(c->st, q->ev_xdone, 0));
+      }
+    }
+    bool ok = true;
+    for (lpfem_ctx* c : g) {  // phase 3: coarse step ahead, verdicts
+      cur = c;
+      if (c->D == 2) step_overlap<2>(c, dt); else step_overlap<3>(c, dt);
+    }
+    for (lpfem_ctx* c : g) {
+      cur = c;
+      ok = step_verdict(c) && ok;
+    }
+    lpfem_status st = LPFEM_OK;
+    for (lpfem_ctx* c : g) {  // phase 4: all commit or none
+      try {
+        step_end(c, ok);
+      } catch (const Err& e) {
+        st = fail(c, e);
+      }
+    }
+    return st;
+  } catch (const Err& e) {
+    for (lpfem_ctx* c : g) c->err = e.what();
+    return fail(cur, e);
+  }
+}
+
+lpfem_status lpfem_inject_fault(lpfem_ctx* c, int family, int max_iter) {
+  if (!c || family < 0 || family > 1) return LPFEM_EINVAL;
+  c->fault_maxit[family] = max_iter > 0 ? max_iter : 0;
+  return LPFEM_OK;
 }
 
 lpfem_status lpfem_get_sizes(const lpfem_ctx* c, long long n_nodes_p2[2], long long n_nodes_p1[2]) {
@@ -2193,7 +2658,7 @@ lpfem_status lpfem_get_sizes(const lpfem_ctx* c, long long n_nodes_p2[2], long l
 
 static lpfem_status copy_out(lpfem_ctx* c, double* dst, const double* src, long long n, int on_device) {
   if (!dst) return LPFEM_OK;
-  cudaError_t e = cudaMemcpyAsync(dst, src, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st);
+  cudaError_t e = cpya(dst, src, n * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st);
   if (e != cudaSuccess) {
     c->err = cudaGetErrorString(e);
     return LPFEM_ECUDA;
@@ -2205,7 +2670,9 @@ lpfem_status lpfem_get_fields(lpfem_ctx* c, double* pF, double* pf, double* pm, 
                               int root) {
   if (!c) return LPFEM_EINVAL;
   if (root < 0 || root >= c->dist.world) return LPFEM_EINVAL;
+  Counted cnt(c);
   try {
+    CK(cudaSetDevice(c->dist.device));
     gather_root(c, root);
   } catch (const Err& e) {
     return fail(c, e);
@@ -2318,7 +2785,7 @@ lpfem_status lpfem_get_system(lpfem_ctx* c, int family, int local_index, int fie
   if (family == 0 && (field < 0 || field > 2)) return LPFEM_EINVAL;
   const SysDesc& S = F.hs[local_index];
   std::vector<long long> rp(S.nrows + 1);
-  if (cudaMemcpy(rp.data(), F.rowptr + S.row_off, (S.nrows + 1) * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (cpy(rp.data(), F.rowptr + S.row_off, (S.nrows + 1) * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return LPFEM_ECUDA;
   *nrows = S.nrows;
   *nnz = rp[S.nrows] - rp[0];
@@ -2327,12 +2794,12 @@ lpfem_status lpfem_get_system(lpfem_ctx* c, int family, int local_index, int fie
   const long long voff = family == 0 ? field * F.nnz : 0;
   const long long roff = (family == 0 ? field * F.rows : 0) + S.row_off;
   const double* vsrc = family == 0 ? F.val : F.aout;
-  if (col && cudaMemcpy(col, F.col + rp[0], *nnz * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return LPFEM_ECUDA;
-  if (val && cudaMemcpy(val, vsrc + voff + rp[0], *nnz * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (col && cpy(col, F.col + rp[0], *nnz * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return LPFEM_ECUDA;
+  if (val && cpy(val, vsrc + voff + rp[0], *nnz * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
     return LPFEM_ECUDA;
-  if (rhs && cudaMemcpy(rhs, F.rhs + roff, S.nrows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (rhs && cpy(rhs, F.rhs + roff, S.nrows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
     return LPFEM_ECUDA;
-  if (x && cudaMemcpy(x, F.x + roff, S.nrows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) return LPFEM_ECUDA;
+  if (x && cpy(x, F.x + roff, S.nrows * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) return LPFEM_ECUDA;
   return LPFEM_OK;
 }
 
@@ -2348,6 +2815,45 @@ lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, dou
     double* y = family == 0 ? F.q : F.W;
     constexpr int NT = 512;
     int tpr = family == 0 ? (c->D == 2 ? 4 : 8) : (c->D == 2 ? TPR2 : TPR3);
+    if (family == 1 && F.nbval) {  // the node-blocked operator the GMRES multiplies with
+      const NBMat B{F.nbval, F.nbcol, F.nbvptr, F.nbcptr, F.nblen};
+      int maxi = 0;
+      double bytes = 0.0;
+      for (size_t i = 0; i < F.hk.size(); ++i) {
+        const KSys& K = F.hk[i];
+        maxi = std::max(maxi, K.n2 + K.n1);
+      }
+      bytes = 8.0 * F.nnz + 4.0 * F.nb_ncols + 24.0 * F.nb_items + 16.0 * F.rows;
+      const int ipc = 4 * NT / tpr;
+      const dim3 grid((maxi + ipc - 1) / ipc, (unsigned)F.hk.size());
+      void* fb = nullptr;
+      const size_t fbytes = 512u << 20;
+      if (flush) CK(cudaMalloc(&fb, fbytes));
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      double tot = 0.0;
+      for (int r = 0; r < reps; ++r) {
+        if (flush) CK(cudaMemsetAsync(fb, r & 0xff, fbytes, c->st));
+        CK(cudaEventRecord(e0, c->st));
+        if (c->D == 2)
+          k_spmv_nb_family<NT, TPR2, 2><<<grid, NT, 0, c->st>>>(F.dk, B, F.rhs, F.W, ipc);
+        else
+          k_spmv_nb_family<NT, TPR3, 3><<<grid, NT, 0, c->st>>>(F.dk, B, F.rhs, F.W, ipc);
+        CKL();
+        CK(cudaEventRecord(e1, c->st));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        tot += ms;
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      if (fb) cudaFree(fb);
+      *ms_per_rep = tot / reps;
+      *bytes_per_rep = bytes;
+      return LPFEM_OK;
+    }
     if (getenv("LPFEM_SPMV_TPR")) tpr = atoi(getenv("LPFEM_SPMV_TPR"));  // experiment
     const int rpc = 4 * NT / tpr;
     int maxr = 0;
@@ -2406,21 +2912,40 @@ lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, dou
   }
 }
 
-lpfem_status lpfem_halo_plan(int dim, const int n_cells[3], const int subdomain_grid[3], int overlap_cells, int rank,
-                             int world, int vertex_only, int kind, int peer, int* out, long long* n_out) {
-  if (!n_cells || !subdomain_grid || !n_out || dim < 2 || dim > 3 || world < 1 || rank < 0 || rank >= world ||
-      peer < 0 || peer >= world || kind < 0 || kind > 2)
-    return LPFEM_EINVAL;
-  RegionGrid G{};
-  G.d = dim;
-  for (int a = 0; a < 3; ++a) {
-    G.n[a] = a < dim ? n_cells[a] : 1;
-    G.m[a] = a < dim ? subdomain_grid[a] : 1;
-    if (a < dim && (G.m[a] < 1 || G.n[a] % G.m[a])) return LPFEM_EMISALIGN;
+static bool plan_grids(int dim, const int* ncp, const int* ncc, const int* grid, int ov, RegionGrid& Gp, RegionGrid& Gc) {
+  if (!ncp || !ncc || !grid || dim < 2 || dim > 3 || ov < 0) return false;
+  for (RegionGrid* G : {&Gp, &Gc}) {
+    const int* n = G == &Gp ? ncp : ncc;
+    G->d = dim;
+    G->ov = ov;
+    for (int a = 0; a < 3; ++a) {
+      G->n[a] = a < dim ? n[a] : 1;
+      G->m[a] = a < dim ? grid[a] : 1;
+      if (a < dim && (G->m[a] < 1 || G->n[a] < 1 || G->n[a] % G->m[a])) return false;
+    }
   }
-  G.ov = overlap_cells;
+  return true;
+}
+
+lpfem_status lpfem_placement(int dim, const int n_cells_p[3], const int n_cells_c[3], const int subdomain_grid[3],
+                             int overlap_cells, int world, int* rank_of_pos) {
+  RegionGrid Gp{}, Gc{};
+  if (world < 1 || !rank_of_pos || !plan_grids(dim, n_cells_p, n_cells_c, subdomain_grid, overlap_cells, Gp, Gc))
+    return LPFEM_EINVAL;
+  const std::vector<int> r = placement(Gp, Gc, world);
+  std::copy(r.begin(), r.end(), rank_of_pos);
+  return LPFEM_OK;
+}
+
+lpfem_status lpfem_halo_plan(int dim, const int n_cells_p[3], const int n_cells_c[3], const int subdomain_grid[3],
+                             int overlap_cells, int region, int rank, int world, int vertex_only, int kind, int peer,
+                             int* out, long long* n_out) {
+  RegionGrid Gp{}, Gc{};
+  if (!n_out || world < 1 || rank < 0 || rank >= world || peer < 0 || peer >= world || kind < 0 || kind > 2 ||
+      region < 0 || region > 1 || !plan_grids(dim, n_cells_p, n_cells_c, subdomain_grid, overlap_cells, Gp, Gc))
+    return LPFEM_EINVAL;
   HaloPlan P;
-  plan_region(G, rank, world, vertex_only != 0, P);
+  plan_region(region == 0 ? Gp : Gc, placement(Gp, Gc, world), rank, world, vertex_only != 0, P);
   const std::vector<int>& v = kind == 0 ? P.need[peer] : (kind == 1 ? P.give[peer] : P.owned[peer]);
   *n_out = (long long)v.size();
   if (out) std::copy(v.begin(), v.end(), out);
@@ -2452,7 +2977,24 @@ void lpfem_destroy(lpfem_ctx* c) {
     for (void* p : xp)
       if (p) cudaFree(p);
   }
+  for (auto* v : {&c->own_p, &c->own_c2, &c->own_c1})
+    for (int* p : *v)
+      if (p) cudaFree(p);
   if (c->gbuf) cudaFree(c->gbuf);
+  if (c->dok) cudaFree(c->dok);
+  if (!c->group_key.empty()) {  // leave the local group
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    auto it = g_groups.find(c->group_key);
+    if (it != g_groups.end()) {
+      for (auto& q : it->second)
+        if (q == c) q = nullptr;
+      bool empty = true;
+      for (auto* q : it->second) empty = empty && !q;
+      if (empty) g_groups.erase(it);
+    }
+  }
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_xdone) cudaEventDestroy(c->ev_xdone);
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   if (c->st2) cudaStreamSynchronize(c->st2);
   if (c->st3) cudaStreamSynchronize(c->st3);
@@ -2464,6 +3006,16 @@ void lpfem_destroy(lpfem_ctx* c) {
   }
   if (c->sol) cusolverDnDestroy(c->sol);
   if (c->sol2) cusolverDnDestroy(c->sol2);
+  for (int k = 0; k < lpfem_ctx::NSI; ++k) {
+    if (c->sinv[k]) cudaStreamSynchronize(c->sinv[k]);
+    if (c->hinv[k]) cusolverDnDestroy(c->hinv[k]);
+    if (c->sinv[k]) cudaStreamDestroy(c->sinv[k]);
+    void* q[] = {c->lwki[k], c->lpivi[k], c->linfoi[k]};
+    for (void* p : q)
+      if (p) cudaFree(p);
+  }
+  for (int k = 0; k <= lpfem_ctx::NSI; ++k)
+    if (c->einv[k]) cudaEventDestroy(c->einv[k]);
   if (c->st2) {
     cudaStreamSynchronize(c->st2);
     cudaStreamDestroy(c->st2);
@@ -2473,8 +3025,10 @@ void lpfem_destroy(lpfem_ctx* c) {
     if (c->evp[i]) cudaEventDestroy(c->evp[i]);
   for (int i = 0; i < 3; ++i)
     if (c->evc[i]) cudaEventDestroy(c->evc[i]);
+  for (int i = 0; i < 2; ++i)
+    if (c->evcp[i]) cudaEventDestroy(c->evcp[i]);
   void* ptrs[] = {c->dense, c->dwork, c->piv, c->dinfo, c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
-                  c->comp_p, c->kmult, c->ref};
+                  c->comp_p, c->comp2[0], c->comp2[1], c->comp2[2], c->comp2_u, c->comp2_p, c->kmult, c->ref, c->convt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int i = 0; i < 4; ++i) {

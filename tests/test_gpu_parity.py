@@ -90,6 +90,17 @@ def test_parity_injection_lognormal_small_2d():
     run_pair(cfg)
 
 
+def test_parity_injection_lognormal_3d_full_trajectory():
+    """cfg4's structure at a size the oracle marches in test time: 3D injection (C16: the biquadratic inflow on
+    z = 2, no-slip sides) with the seeded log-normal permeability per porous coarse cell (C15, seed 4: the
+    multiplier enters the porous operators and the BJ friction / tangential Gamma terms of the conduit boxes
+    touching Gamma), 2x2x2 subdomains per region, both regions, every step to t_4 (the lag chain makes
+    p_F, p_f, p_m non-zero from steps 2, 3, 4)."""
+    cfg = I.make_config(dim=3, H=1 / 4, h=1 / 8, grid=2, dt=0.01, steps=4, problem="injection", seed=4)
+    worst, st = run_pair(cfg)
+    print("3d injection lognormal worst", worst)
+
+
 def test_parity_3d_small_mms():
     cfg = I.make_config(dim=3, H=1 / 2, h=1 / 4, grid=2, dt=0.1, steps=2, problem="mms")
     run_pair(cfg)

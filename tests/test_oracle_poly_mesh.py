@@ -172,8 +172,9 @@ def test_node_class_precedence_2d():
     assert list(cls) == [M.DIR, M.GAMMA, M.DIR, M.ART, M.ART, M.DIR, M.INT]
 
 
-def test_prolongation_weights_exact():
-    """Exact rational weights reproduce P2 interpolation of a quadratic at a fine node (nesting)."""
+def test_prolongation_weights_partition_of_unity():
+    """Exact rational weights sum to one (constants reproduced); quadratic reproduction is pinned by
+    tests/test_oracle_pins_r2.py::test_prolongation_weights_reproduce_quadratics."""
     for d, R in ((2, 4), (3, 3)):
         for num in itertools.product(range(2 * R + 1), repeat=d):
             w = exact_prolong_weights(d, num, R)
