@@ -94,6 +94,12 @@ typedef struct {
                            counts, identical on every rank and for every world size, so the fields are bitwise
                            identical for any world (cost: at world N a rank's Krylov launches
                            use about 1/N of the SMs the per-rank choice would use) */
+  int algorithm;        /* 3 (or 0, default): Algorithm 3, the local parallel method.
+                           1: Algorithm 1, partitioned time stepping on the fine mesh T_h, the paper's
+                           comparison scheme.  With H == h it runs on the dense coarse-step path (small meshes);
+                           with H > h the subdomain grid must be 1 and the overlap 0: the whole regions are solved
+                           by the fine stage's batched multilevel Krylov kernels (H sets the coarsest preconditioner
+                           level), the Navier-Stokes step by Newton iterations to the C11 test */
 } lpfem_opts;
 
 enum { LPFEM_TRANSPORT_NCCL = 0,    /* one process per GPU; halo exchange by NCCL grouped send/recv (default) */

@@ -51,7 +51,8 @@ class Data(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("lag_mode", C.c_int), ("krylov_rtol", C.c_double), ("max_iter", C.c_int), ("gmres_restart", C.c_int),
-                ("picard_rtol", C.c_double), ("picard_max", C.c_int), ("world_invariant", C.c_int)]
+                ("picard_rtol", C.c_double), ("picard_max", C.c_int), ("world_invariant", C.c_int),
+                ("algorithm", C.c_int)]
 
 
 class Dist(C.Structure):
@@ -144,7 +145,8 @@ class LPFEM:
                    const_value=cfg.get("const_value", 1.0))
         o = Opts(lag_mode=LAG[cfg.get("lag_mode", "composite")], krylov_rtol=cfg.get("krylov_rtol", 1e-12),
                  max_iter=max_iter, gmres_restart=0, picard_rtol=cfg.get("picard_rtol", 1e-13),
-                 picard_max=cfg.get("picard_max", 50), world_invariant=int(world_invariant))
+                 picard_max=cfg.get("picard_max", 50), world_invariant=int(world_invariant),
+                 algorithm=int(cfg.get("algorithm", 3)))
         ds = Dist(rank=rank, world=world, device=device, cuda_stream=stream, transport=TRANSPORT[transport])
         if nccl_id is not None:
             C.memmove(ds.nccl_id, nccl_id, 128)

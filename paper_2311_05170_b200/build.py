@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "lpfem.cu")
-OUT = os.path.join(HERE, "liblpfem.so")
+OUT = os.environ.get("LPFEM_BUILD_OUT") or os.path.join(HERE, "liblpfem.so")  # override: experiment variants
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

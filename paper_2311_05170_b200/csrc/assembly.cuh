@@ -353,7 +353,9 @@ __device__ double prolong_p1(const double* __restrict__ pc, const int nH[3], int
 struct PorousPrepArgs {
   const double* coarse_new[3];   // coarse porous state at n+1 (fine stage) or n (coarse stage)
   const double* coarse_old[3];   // coarse porous state at n
-  const double* coarse_u_old;    // coarse conduit velocity at n, last component (for the flux)
+  const double* coarse_u_old;    // conduit velocity at n, last component (for the flux): coarse, or (Algorithm 1
+                                 // on T_h) the fine composite
+  int nHu[3], Ru;                // cells of that velocity's mesh per axis and fine cells per cell of it
   const double* comp[3];         // global fine composite (mode B)
   const double* ecorr;           // mode A stored corrections (3 fields, row space) or NULL
   int nHp[3], nHc[3];            // coarse cells of porous / conduit regions
@@ -403,7 +405,7 @@ __global__ void k_porous_prep(const SysDesc* __restrict__ sys, Level L, ProbData
   if (g[D - 1] == L.G.gamma_g) {
     int gc[3] = {g[0], g[1], g[2]};
     gc[D - 1] = A.conduit_gamma_g;
-    w = -prolong_p2<D>(A.coarse_u_old, A.nHc, A.Rp, gc);
+    w = -prolong_p2<D>(A.coarse_u_old, A.nHu, A.Ru, gc);
   }
   wg[k0] = w;
 }

@@ -44,17 +44,6 @@ struct RefT {
   double TF[NF][NF][LF];       // facet: int phi_i dphi_j/dlam_l
 };
 
-// Convection tensors per Kuhn simplex type on the unit cell (cell sizes 1), built on the host from C3 and the
-// barycentric gradients G^_t (kuhn_grad with h = 1); the level's cell sizes enter as G = G^_t / h per axis:
-//   Q^[t][i][c][j][m] = sum_k C3[i][m][j][k] G^_t[k][c]   -> eta int phi_i (W.grad) phi_j = eta |K| sum_{c,m} W_c(m) Q^/h_c
-//   T^[t][i][b][j][m] = sum_k C3[i][j][m][k] G^_t[k][b]   -> eta int phi_i phi_j d_b U_a = eta |K| sum_m U_a(m) T^/h_b
-template <int D>
-struct ConvT {
-  static constexpr int N = n2_of(D), NT = nt_of(D);
-  double Q[NT][N][D][N][N];
-  double T[NT][N][D][N][N];
-};
-
 // One region (porous or conduit) at one level (coarse T_H or fine T_h).
 struct LevelGeom {
   int n[3];        // cells per axis

@@ -256,237 +256,198 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
   }
 }
 
-// Per-step operator: A' = mask * (A_const + eta N(W) [+ eta R(U)]) * diag(s) and right-hand side
-// rhs = mask * (b_load - A z), b_load = eta M f + (eta/dt) M u~^n [+ eta N(U) U] + Gamma loads.
-// 254 registers in 3D (low occupancy) is the measured optimum: forcing 2 or 3 blocks of 256 per SM spills and
-// runs 5% / 24% slower (cfg4 226 -> 236 / 280 ms)
-#ifndef LPFEM_CSTEP_MINB
-#define LPFEM_CSTEP_MINB 1
-#endif
-template <int D>
-__global__ void __launch_bounds__(256, LPFEM_CSTEP_MINB)
-k_conduit_step(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int newton,
-                               const double* __restrict__ kmult, int nHp0, int nHp1, int nHp2,
-                               const RefT<D>* __restrict__ ref, const long long* __restrict__ rowptr,
-                               const int* __restrict__ col, const double* __restrict__ aconst,
-                               const double* __restrict__ s, const double* __restrict__ z,
-                               const double* __restrict__ W, const double* __restrict__ lag,
-                               const double* __restrict__ f, const double* __restrict__ pfg,
-                               double* __restrict__ aout, double* __restrict__ rhs) {
-  const SysDesc S = sys[blockIdx.y];
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
-  constexpr int N = n2_of(D);
-  // the convection tensor in shared memory: every thread reads C3[i] slabs for its own local node i (divergent
-  // across the warp), which from L1 serialised into one wavefront per distinct line
-  constexpr int NC3 = N * N * N * (D + 1);
-  __shared__ double sC3[NC3];
-  if ((int)(blockIdx.x * blockDim.x) >= S.nrows) return;  // block-uniform
-  for (int k = threadIdx.x; k < NC3; k += blockDim.x) sC3[k] = (&ref->C3[0][0][0][0])[k];
-  __syncthreads();
-  if (r >= S.nrows) return;
-  auto C3 = [&](int i, int m, int j, int k) -> double { return sC3[((i * N + m) * N + j) * (D + 1) + k]; };
-  const int nHp[3] = {nHp0, nHp1, nHp2};
-  const long long o = S.row_off;
-  const long long rb = rowptr[o + r], re = rowptr[o + r + 1];
-  const double* zs = z + o;
-  const double* ss = s + o;
-  for (long long q = rb; q < re; ++q) aout[q] = aconst[q];
-  double b = 0.0;
-  if (r < D * S.n2) {
-    const int a = r / S.n2;
-    int l[3] = {0, 0, 0};
-    unlex<D>(r % S.n2, S.np, l);
-    const long long Ln = block_len(col, rb, re, S.n2);
-    const double vol = kuhn_volume<D>(L.G.hc);
-    const double* Ws = W + o;
-    const double* Ls = lag + o + a * S.n2;
-    const double* Fs = f + o + a * S.n2;
-    for_simplices_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
-      double G[D + 1][D];
-      kuhn_grad<D>(c_kt[D].perm[t], L.G.hc, G);
-      int idx[N];
-      double We[D][N];
-      for (int j = 0; j < N; ++j) {
-        int v[3];
-        for (int e = 0; e < D; ++e) v[e] = 2 * c[e] + c_kt[D].off[t][j][e];
-        idx[j] = (int)lex<D>(v, S.np);
-        for (int e = 0; e < D; ++e) We[e][j] = Ws[e * S.n2 + idx[j]];
-      }
-      // w_l(m) = W(m) . grad lam_l
-      double wl[D + 1][N];
-      for (int k = 0; k <= D; ++k)
-        for (int m = 0; m < N; ++m) {
-          double s2 = 0.0;
-          for (int e = 0; e < D; ++e) s2 += We[e][m] * G[k][e];
-          wl[k][m] = s2;
-        }
-      const double ev = cc.eta * vol;
-      for (int j = 0; j < N; ++j) {
-        const long long p0 = find_slot(col, rb, rb + Ln, idx[j]);
-        // convection eta int phi_i (W.grad phi_j)
-        double cv = 0.0;
-        for (int k = 0; k <= D; ++k)
-          for (int m = 0; m < N; ++m) cv += C3(i, m, j, k) * wl[k][m];
-        cv *= ev;
-        aout[p0 + a * Ln] += cv;
-        b += vol * ref->M22[i][j] * (cc.eta * Fs[idx[j]] + (cc.eta / cc.dt) * Ls[idx[j]]);
-        if (newton) {
-          b += cv * We[a][j];  // eta ((U.grad)U, v)
-          // reaction eta int phi_i phi_j d_b U_a = eta sum_m U_a(m) sum_k C3[i][j][m][k] G[k][b]
-          for (int bb = 0; bb < D; ++bb) {
-            double rv = 0.0;
-            for (int m = 0; m < N; ++m) {
-              double t2 = 0.0;
-              for (int k = 0; k <= D; ++k) t2 += C3(i, j, m, k) * G[k][bb];
-              rv += We[a][m] * t2;
-            }
-            aout[p0 + bb * Ln] += ev * rv;
-          }
-        }
-      }
-    });
-    if (S.has_gamma && 2 * S.c0[D - 1] + l[D - 1] == L.G.gamma_g) {
-      double hf[3] = {L.G.hc[0], L.G.hc[1], 0};
-      const double fvol = kuhn_volume<D - 1>(hf);
-      const double* P = pfg + o;
-      for_facets_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
-        const double kF = cc.kF * gamma_mult<D>(kmult, L, S, c, nHp);
-        double Gt[D][D - 1];
-        double hf2[3] = {L.G.hc[0], L.G.hc[1], 0};
-        kuhn_grad<D - 1>(c_kt[D - 1].perm[t], hf2, Gt);
-        for (int j = 0; j < n2_of(D - 1); ++j) {
-          int v[3] = {0, 0, 0};
-          for (int e = 0; e < D - 1; ++e) v[e] = 2 * c[e] + c_kt[D - 1].off[t][j][e];
-          v[D - 1] = l[D - 1];
-          const double pj = P[lex<D>(v, S.np)];
-          if (a == D - 1) {
-            b += (cc.eta / cc.rho) * fvol * ref->MF[i][j] * pj;  // -(eta/rho)<p_F, v.n_c>, n_c = -e_last
-          } else {
-            const double ct = cc.eta * cc.nu * cc.alpha * sqrt(kF) / cc.mu;
-            double tg = 0.0;
-            for (int k = 0; k < D; ++k) tg += ref->TF[i][j][k] * Gt[k][a];
-            b -= ct * fvol * tg * pj;  // -(eta nu alpha sqrt(k_F)/mu)<grad_tau p_F, P_tau v>
-          }
-        }
-      });
-    }
-  }
-  for (long long q = rb; q < re; ++q) b -= aout[q] * zs[col[q]];
-  const bool fixed = ss[r] == 0.0;
-  for (long long q = rb; q < re; ++q) aout[q] = fixed ? 0.0 : aout[q] * ss[col[q]];
-  rhs[o + r] = fixed ? 0.0 : b;
-}
-
-// Per-step operator, node-based: one thread per velocity P2 node assembles the D rows of that node together (one
-// column search per element node, the convection term eta((W.grad)e, v) computed once for all D components and the
-// Newton reaction eta((e.grad)U, v) from the per-type tensors: ~1.2k FMA per element visit instead of ~5k for a
-// row-per-thread walk); one thread per P1 vertex copies, masks and scales its continuity row.
+// Per-step operator, one WARP per velocity P2 node (all D rows of the node) or per continuity row.  Everything the
+// element walk touches is staged in shared memory first, with independent coalesced loads: the node's rows of
+// aconst, its column list, and the wind W and the load (eta f + (eta/dt) u~^n) at its P2 neighbours -- the nodes of
+// all simplices around it.  Every simplex then adds its convection / Newton-reaction block in one conflict-free
+// round (lane = (j, b): element node j, column block b; distinct lanes hit distinct entries; the position of node j
+// in the row by binary search in the staged column list), and the finished rows are masked, scaled and written once
+// (coalesced): one read of aconst, one write of aout, no global access inside the walk.  Barycentric gradients of
+// Kuhn simplices are +-1/h per axis: sum_k C3[..][k] G[k][c] = (C3[..][p + 1] - C3[..][p]) / h_c with p the rank of
+// axis c in the simplex's permutation (C3 in shared memory).
 //   A' = mask * (A_const + eta N(W) [+ eta R(U)]) * diag(s)
 //   rhs = mask * (b_load - A z), b_load = eta M f + (eta/dt) M u~^n [+ eta N(U) U] + Gamma loads.
 template <int D>
-__global__ void __launch_bounds__(128)
-k_conduit_step_nb(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int newton,
-                  const double* __restrict__ kmult, int nHp0, int nHp1, int nHp2, const RefT<D>* __restrict__ ref,
-                  const ConvT<D>* __restrict__ ct, const long long* __restrict__ rowptr, const int* __restrict__ col,
-                  const double* __restrict__ aconst, const double* __restrict__ s, const double* __restrict__ z,
-                  const double* __restrict__ W, const double* __restrict__ lag, const double* __restrict__ f,
-                  const double* __restrict__ pfg, double* __restrict__ aout, double* __restrict__ rhs) {
-  const SysDesc S = sys[blockIdx.y];
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= S.n2 + S.n1) return;
+struct CStepW;
+template <int D, int WPB>
+constexpr size_t cstep_smem() {  // DA, DB (D x N^3 each), M22 (N^2), one CStepW per warp
+  return sizeof(double) * (2 * D * n2_of(D) * n2_of(D) * n2_of(D) + n2_of(D) * n2_of(D)) + WPB * sizeof(CStepW<D>);
+}
+template <int D>
+struct CStepW {
+  static constexpr int N = n2_of(D);
+  static constexpr int RMAX = D == 3 ? 232 : 56;  // >= longest velocity row (checked at setup): 3 x 65 + 27 / 2 x 19 + 9
+  static constexpr int LMAX = D == 3 ? 72 : 24;   // >= P2 neighbours of a node
+  double row[D][RMAX];  // the node's D rows
+  double Uw[D][LMAX];   // wind at the P2 neighbours (row order)
+  double Lw[D][LMAX];   // eta f + (eta/dt) u~^n at the P2 neighbours
+  int colr[RMAX];       // column list of the rows (block 0: P2 neighbours, ascending)
+  int slot[N];          // position of the current simplex's nodes in the neighbour list
+};
+
+template <int D, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int newton,
+                 const double* __restrict__ kmult, int nHp0, int nHp1, int nHp2, const RefT<D>* __restrict__ ref,
+                 const long long* __restrict__ rowptr, const int* __restrict__ col,
+                 const double* __restrict__ aconst, const double* __restrict__ s, const double* __restrict__ z,
+                 const double* __restrict__ W, const double* __restrict__ lag, const double* __restrict__ f,
+                 const double* __restrict__ pfg, double* __restrict__ aout, double* __restrict__ rhs) {
   constexpr int N = n2_of(D);
+  constexpr int NT3 = D * N * N * N;
+  // barycentric-gradient differences of C3 (gradients of Kuhn simplices are +-1/h: sum_k C3[..][k] G[k][c] =
+  // (C3[..][p + 1] - C3[..][p]) / h_c, p = rank of axis c in the simplex's permutation), element node j fastest so
+  // that the lanes (j, .) of a warp read consecutive words:
+  //   DA[p][i][m][j] = C3[i][m][j][p+1] - C3[i][m][j][p]   (convection: phi_i phi_m d_c phi_j)
+  //   DB[p][i][m][j] = C3[i][j][m][p+1] - C3[i][j][m][p]   (reaction:   phi_i phi_j d_c phi_m)
+  extern __shared__ __align__(16) double cstep_dyn[];  // DA, DB, M22, then one CStepW per warp (cstep_smem bytes)
+  double* DA = cstep_dyn;
+  double* DB = cstep_dyn + NT3;
+  double* sM = cstep_dyn + 2 * NT3;
+  CStepW<D>* wb = reinterpret_cast<CStepW<D>*>(cstep_dyn + 2 * NT3 + N * N);
+  const SysDesc S = sys[blockIdx.y];
+  const int nitems = S.n2 + S.n1;
+  if ((int)(blockIdx.x * WPB) >= nitems) return;  // block-uniform
+  for (int k = threadIdx.x; k < NT3; k += blockDim.x) {
+    const int j = k % N, m = (k / N) % N, i = (k / (N * N)) % N, p = k / (N * N * N);
+    DA[k] = ref->C3[i][m][j][p + 1] - ref->C3[i][m][j][p];
+    DB[k] = ref->C3[i][j][m][p + 1] - ref->C3[i][j][m][p];
+  }
+  for (int k = threadIdx.x; k < N * N; k += blockDim.x) sM[k] = (&ref->M22[0][0])[k];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * WPB + w;
+  if (r >= nitems) return;
   const long long o = S.row_off;
   const double* zs = z + o;
   const double* ss = s + o;
   if (r >= S.n2) {  // continuity row: constant (eta (q, div u)), masked and scaled
     const long long row = o + D * S.n2 + (r - S.n2);
     const long long rb = rowptr[row], re = rowptr[row + 1];
-    double b = 0.0;
-    for (long long q = rb; q < re; ++q) b -= aconst[q] * zs[col[q]];
     const bool fixed = ss[D * S.n2 + (r - S.n2)] == 0.0;
-    for (long long q = rb; q < re; ++q) aout[q] = fixed ? 0.0 : aconst[q] * ss[col[q]];
-    rhs[row] = fixed ? 0.0 : b;
+    double b = 0.0;
+    for (long long q = rb + lane; q < re; q += 32) {
+      const double v = aconst[q];
+      const int cq = col[q];
+      b -= v * zs[cq];
+      aout[q] = fixed ? 0.0 : v * ss[cq];
+    }
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) b += __shfl_xor_sync(0xffffffffu, b, k);
+    if (lane == 0) rhs[row] = fixed ? 0.0 : b;
     return;
   }
+  CStepW<D>& B = wb[w];
   const int nHp[3] = {nHp0, nHp1, nHp2};
   int l[3] = {0, 0, 0};
   unlex<D>(r, S.np, l);
-  long long rb[D], re[D];
+  long long rb[D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    rb[a] = rowptr[o + a * S.n2 + r];
-    re[a] = rowptr[o + a * S.n2 + r + 1];
-  }
-  const long long Ln = block_len(col, rb[0], re[0], S.n2);  // same column structure in all D rows of the node
+  for (int a = 0; a < D; ++a) rb[a] = rowptr[o + a * S.n2 + r];
+  const int RL = (int)(rowptr[o + r + 1] - rb[0]);  // the D rows of a node have the same length and columns
+  const double* Ws = W + o;
+  const double* Ls = lag + o;
+  const double* Fs = f + o;
+  // stage: columns, rows of aconst, wind and loads at the P2 neighbours (independent loads, one latency)
+  for (int q = lane; q < RL; q += 32) B.colr[q] = col[rb[0] + q];
 #pragma unroll
   for (int a = 0; a < D; ++a)
-    for (long long q = rb[a]; q < re[a]; ++q) aout[q] = aconst[q];
-  double b[D];
+    for (int q = lane; q < RL; q += 32) B.row[a][q] = aconst[rb[a] + q];
+  __syncwarp();
+  int Ln = 0;  // P2 neighbours: columns < n2 (ascending), ballot over the staged list
+  for (int q0 = 0; q0 < RL; q0 += 32) {
+    const bool in = q0 + lane < RL && B.colr[q0 + lane] < S.n2;
+    Ln += __popc(__ballot_sync(0xffffffffu, in));
+  }
 #pragma unroll
-  for (int a = 0; a < D; ++a) b[a] = 0.0;
+  for (int a = 0; a < D; ++a)
+    for (int q = lane; q < Ln; q += 32) {
+      const int cq = B.colr[q];
+      B.Uw[a][q] = Ws[a * S.n2 + cq];
+      B.Lw[a][q] = cc.eta * Fs[a * S.n2 + cq] + (cc.eta / cc.dt) * Ls[a * S.n2 + cq];
+    }
   const double vol = kuhn_volume<D>(L.G.hc);
   const double ev = cc.eta * vol;
   double ih[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) ih[a] = 1.0 / L.G.hc[a];
-  const double* Ws = W + o;
-  const double* Ls = lag + o;
-  const double* Fs = f + o;
+  // lane (j, bb): element node j, column block bb (also the component whose right-hand side it accumulates)
+  const int jl = lane / D, bl = lane % D;
+  const bool act = lane < N * D;
+  double bpart = 0.0;
+  __syncwarp();
   for_simplices_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
-    int idx[N];
-    double Ue[D][N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
+    if (lane < N) {  // slot of element node m in the neighbour list (binary search in shared memory)
       int v[3];
-      for (int e = 0; e < D; ++e) v[e] = 2 * c[e] + c_kt[D].off[t][j][e];
-      idx[j] = (int)lex<D>(v, S.np);
-#pragma unroll
-      for (int e = 0; e < D; ++e) Ue[e][j] = Ws[e * S.n2 + idx[j]];
-    }
-    const double* Qi = &ct->Q[t][i][0][0][0];
-    const double* Ti = &ct->T[t][i][0][0][0];
-    for (int j = 0; j < N; ++j) {
-      const long long p0 = find_slot(col, rb[0], rb[0] + Ln, idx[j]) - rb[0];
-      // convection eta int phi_i (W.grad phi_j), identical for the D components
-      double cv = 0.0;
-#pragma unroll
-      for (int e = 0; e < D; ++e) {
-        const double* q = Qi + (e * N + j) * N;
-        double se = 0.0;
-#pragma unroll
-        for (int m = 0; m < N; ++m) se += Ue[e][m] * q[m];
-        cv += se * ih[e];
+      for (int a = 0; a < D; ++a) v[a] = 2 * c[a] + c_kt[D].off[t][lane][a];
+      const int key = (int)lex<D>(v, S.np);
+      int lo = 0, hi = Ln;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (B.colr[mid] < key) lo = mid + 1; else hi = mid;
       }
+      B.slot[lane] = lo;
+    }
+    __syncwarp();
+    // lane (j, e): se_e(j) = sum_m W_e(m) DA[p_e][i][m][j] / h_e; cv(j) = eta |K| sum_e se_e(j) (the D lanes of node j
+    // exchange their terms, fixed order); the reaction of column block e from DB[p_e]
+    double ue[D][N];
+    int sl[N];
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      sl[m] = B.slot[m];
+#pragma unroll
+      for (int a = 0; a < D; ++a) ue[a][m] = B.Uw[a][sl[m]];
+    }
+    const int j = act ? jl : 0;
+    const int p = c_kt[D].pos[t][bl];
+    const double* da = DA + ((p * N + i) * N) * N + j;
+    const double* db = DB + ((p * N + i) * N) * N + j;
+    double se = 0.0;
+    if (act) {
+      const double* ub = B.Uw[bl];
+#pragma unroll
+      for (int m = 0; m < N; ++m) se += ub[sl[m]] * da[m * N];
+      se *= 1.0 / L.G.hc[bl];
+    }
+    double cv = 0.0;
+#pragma unroll
+    for (int e = 0; e < D; ++e) cv += __shfl_sync(0xffffffffu, se, jl * D + e);
+    if (act) {
       cv *= ev;
-      const double mij = vol * ref->M22[i][j];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        aout[rb[a] + p0 + a * Ln] += cv;
-        b[a] += mij * (cc.eta * Fs[a * S.n2 + idx[j]] + (cc.eta / cc.dt) * Ls[a * S.n2 + idx[j]]);
-      }
+      const int p0 = B.slot[j];
+      double self = cv;  // entry (row bl, block bl)
       if (newton) {
+        // reaction eta int phi_i phi_j d_bl U_a -> entry (row a, block bl)
+        double tv[N];
 #pragma unroll
-        for (int a = 0; a < D; ++a) b[a] += cv * Ue[a][j];  // eta ((U.grad)U, v)
-        // reaction eta int phi_i phi_j d_bb U_a = eta |K| sum_m U_a(m) T^[t][i][bb][j][m] / h_bb
+        for (int m = 0; m < N; ++m) tv[m] = db[m * N];
+        const double sc = ev / L.G.hc[bl];
 #pragma unroll
-        for (int bb = 0; bb < D; ++bb) {
-          const double* tq = Ti + (bb * N + j) * N;
-          double tv[N];
+        for (int a = 0; a < D; ++a) {
+          double rv = 0.0;
 #pragma unroll
-          for (int m = 0; m < N; ++m) tv[m] = tq[m];
-          const double sc = ev * ih[bb];
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            double rv = 0.0;
-#pragma unroll
-            for (int m = 0; m < N; ++m) rv += Ue[a][m] * tv[m];
-            aout[rb[a] + p0 + bb * Ln] += sc * rv;
-          }
+          for (int m = 0; m < N; ++m) rv += ue[a][m] * tv[m];
+          if (a == bl) self += sc * rv;
+          else B.row[a][p0 + bl * Ln] += sc * rv;
         }
+        bpart += cv * B.Uw[bl][p0];  // eta ((U.grad)U, v), component bl
       }
+      B.row[bl][p0 + bl * Ln] += self;
+      bpart += vol * sM[i * N + j] * B.Lw[bl][p0];
     }
+    __syncwarp();
   });
-  if (S.has_gamma && 2 * S.c0[D - 1] + l[D - 1] == L.G.gamma_g) {
+  // right-hand side per component: lanes with bl == a hold its partial sums (fixed-order shuffle tree)
+  double bsum[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double v = (act && bl == a) ? bpart : 0.0;
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) v += __shfl_xor_sync(0xffffffffu, v, k);
+    bsum[a] = v;
+  }
+  if (S.has_gamma && 2 * S.c0[D - 1] + l[D - 1] == L.G.gamma_g && lane == 0) {
     double hf[3] = {L.G.hc[0], L.G.hc[1], 0};
     const double fvol = kuhn_volume<D - 1>(hf);
     const double* P = pfg + o;
@@ -501,23 +462,29 @@ k_conduit_step_nb(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int
         for (int e = 0; e < D - 1; ++e) v[e] = 2 * c[e] + c_kt[D - 1].off[t][j][e];
         v[D - 1] = l[D - 1];
         const double pj = P[lex<D>(v, S.np)];
-        b[D - 1] += (cc.eta / cc.rho) * fvol * ref->MF[i][j] * pj;  // -(eta/rho)<p_F, v.n_c>, n_c = -e_last
-#pragma unroll
+        bsum[D - 1] += (cc.eta / cc.rho) * fvol * ref->MF[i][j] * pj;  // -(eta/rho)<p_F, v.n_c>, n_c = -e_last
         for (int a = 0; a < D - 1; ++a) {
           double tg = 0.0;
           for (int k = 0; k < D; ++k) tg += ref->TF[i][j][k] * Gt[k][a];
-          b[a] -= ctg * fvol * tg * pj;  // -(eta nu alpha sqrt(k_F)/mu)<grad_tau p_F, P_tau v>
+          bsum[a] -= ctg * fvol * tg * pj;  // -(eta nu alpha sqrt(k_F)/mu)<grad_tau p_F, P_tau v>
         }
       }
     });
   }
+  __syncwarp();
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    double ba = b[a];
-    for (long long q = rb[a]; q < re[a]; ++q) ba -= aout[q] * zs[col[q]];
     const bool fixed = ss[a * S.n2 + r] == 0.0;
-    for (long long q = rb[a]; q < re[a]; ++q) aout[q] = fixed ? 0.0 : aout[q] * ss[col[q]];
-    rhs[o + a * S.n2 + r] = fixed ? 0.0 : ba;
+    double bz = 0.0;
+    for (int q = lane; q < RL; q += 32) {
+      const double v = B.row[a][q];
+      const int cq = B.colr[q];  // the same columns in all D rows of the node
+      bz += v * zs[cq];
+      aout[rb[a] + q] = fixed ? 0.0 : v * ss[cq];
+    }
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) bz += __shfl_xor_sync(0xffffffffu, bz, k);
+    if (lane == 0) rhs[o + a * S.n2 + r] = fixed ? 0.0 : bsum[a] - bz;
   }
 }
 

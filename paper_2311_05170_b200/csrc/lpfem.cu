@@ -215,7 +215,8 @@ struct lpfem_ctx {
   double* cst[3][3] = {};
   double* cu[3] = {};
   double* cp[3] = {};
-  cudaStream_t st2 = nullptr;  // coarse marching stream (overlaps the fine stage)
+  cudaStream_t st2 = nullptr;  // coarse marching stream (overlaps the fine stage), highest priority
+  int prio_hi = 0;
   int nsm = 148;               // SMs of the device
   cudaStream_t st3 = nullptr;  // fine porous stage, concurrent with the fine conduit stage (independent)
   cudaEvent_t evp[3] = {};     // fork / join of st3; [2]: conduit GMRES about to launch (gates the porous PCG)
@@ -247,11 +248,16 @@ struct lpfem_ctx {
   bool pending_ok = true;       // convergence verdict of the step in flight (step_begin .. step_end)
   double pending_t = 0.0;
   double pending_res[2] = {0, 0};
+  // Algorithm 1 on T_h at scale (lpfem_opts.algorithm = 1, H > h): Newton iterates of the fine conduit step and the
+  // iterate injected into the coarse P2 layout (linearisation point of the preconditioner's coarse-box operators)
+  bool alg1k = false;
+  double *a1u[2] = {}, *a1p[2] = {}, *a1uH = nullptr;
+  bool alg1_ok = true;
+  double alg1_gm_ms = 0.0;  // GMRES device time of the Newton iterations of the step in flight
   long long n2p_f = 0, n2c_f = 0, n1c_f = 0, n2p_c = 0, n2c_c = 0, n1c_c = 0;
   double* kmult = nullptr;
   std::vector<double> hkmult;
   void* ref = nullptr;
-  void* convt = nullptr;  // ConvT<D>: per-simplex-type convection tensors (k_conduit_step_nb)
   cudaStream_t st = nullptr;
   cudaEvent_t ev[4] = {};
   cudaEvent_t ek[4] = {};
@@ -501,6 +507,14 @@ void build_nb(lpfem_ctx* c, Family& F) {
   F.nbval = dalloc<double>(F.nnz);
   k_nb_cols<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, F.nbioff, F.rowptr, F.col, F.nblen, F.nbcptr, F.nbcol);
   CKL();
+}
+
+// the warp-per-node conduit assembly keeps a node's rows in shared memory (CStepW<D>::RMAX entries per row)
+template <int D>
+void check_row_len(const Family& F) {
+  long long mx = 0;
+  for (size_t i = 0; i + 1 < F.hrp.size(); ++i) mx = std::max(mx, F.hrp[i + 1] - F.hrp[i]);
+  if (mx > CStepW<D>::RMAX) throw Err(LPFEM_ESTATE, "conduit row longer than the assembly buffer");
 }
 
 void alloc_vectors(lpfem_ctx* c, Family& F, bool level_family = false) {
@@ -869,11 +883,6 @@ ConduitCoefs conduit_coefs(const lpfem_ctx* c, double dt, double hmin) {
 }
 
 template <int D>
-const ConvT<D>* convtp(const lpfem_ctx* c) {
-  return static_cast<const ConvT<D>*>(c->convt);
-}
-
-template <int D>
 const RefT<D>* refp(const lpfem_ctx* c) {
   return (const RefT<D>*)c->ref;
 }
@@ -1051,7 +1060,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.maxit = (C.level == 1 && c->fault_maxit[1] > 0) ? c->fault_maxit[1] : c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
-  a.warm = (C.level == 1 && !c->kn.cold_start) ? std::min(C.solved, c->warm_order) : 0;
+  a.warm = (C.level == 1 && !c->kn.cold_start && !c->alg1k) ? std::min(C.solved, c->warm_order) : 0;
   a.xp = a.warm > 0 ? C.xp : nullptr;
   a.order = C.level == 1 ? C.dorder : nullptr;
   if (C.nbval) {
@@ -1198,6 +1207,18 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
         bytes += k.spmv * (12.0 * nz + 32.0 * rows);
       }
       bytes += kind == 0 ? 64.0 * rows * k.iters : 48.0 * rows * k.iters + 16.0 * rows * k.vsum;
+      // multilevel preconditioner, once per iteration: the fine vector read by the restriction and by the fine
+      // combine, the fine scaling, the result (32 B/row); every level's restricted vector, scaling and correction
+      // (~40 B per level row, the transfers' gathers hit the cache); the dense coarse-box inverse (fp32 conduit,
+      // fp64 porous: 4 / 8 B per entry)
+      const int nl = kind == 0 ? c->nlp : c->nl;
+      if (nl > 0) {
+        const Family* lv = kind == 0 ? c->plv : c->lvl;
+        double lrows = 0.0;
+        for (int l = 0; l < nl; ++l) lrows += lv[l].hs[s].nrows;
+        const double nL = lv[nl - 1].hs[s].nrows;
+        bytes += k.iters * (32.0 * rows + 40.0 * lrows + (kind == 0 ? 8.0 : 4.0) * nL * nL);
+      }
     }
     c->stats.bytes_krylov[kind] += bytes;
     c->stats.krylov_launches[kind] += 1;
@@ -1205,9 +1226,11 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
   }
 }
 
+// alg1: Algorithm 1 on T_h (lpfem_opts.algorithm = 1): base and lagged state from the fine composite at the same
+// level (mode 2 indexing), the Gamma flux from the fine composite velocity (eq. fullypF)
 template <int D>
 void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* const* cold, const double* cu_old_last,
-                  double* const* out) {
+                  double* const* out, bool alg1 = false) {
   Family& P = c->fam[lev][0];
   const int ns = (int)P.hs.size();
   if (!ns) return;
@@ -1229,6 +1252,14 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
   A.conduit_gamma_g = 0;
   A.mode = lev == 0 ? 2 : (c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN ? 1 : 0);
   A.t = t;
+  for (int a = 0; a < 3; ++a) A.nHu[a] = A.nHc[a];
+  A.Ru = A.Rp;
+  if (alg1) {
+    A.mode = 2;
+    A.Rp = 1;
+    A.Ru = 1;
+    for (int a = 0; a < 3; ++a) A.nHu[a] = c->nf_c[a];
+  }
   k_porous_prep<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, c->Lp[lev], c->pd, c->co, A, P.base, P.z, P.lag,
                                                               P.qf, P.aux, P.rows);
   CKL();
@@ -1244,6 +1275,24 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
   k_porous_writeback<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(
       P.ds, c->Lp[lev], P.z, P.x, P.isq, P.base, P.ecorr2, out[0], out[1], out[2], 2 * c->Lp[lev].G.n[0] + 1,
       2 * c->Lp[lev].G.n[1] + 1, 2 * c->Lp[lev].G.n[2] + 1, P.rows);
+  CKL();
+}
+
+// per-step conduit operator and right-hand side of a family (conduit.cuh k_conduit_step_w: one warp per node / row)
+template <int D>
+void conduit_step(cudaStream_t st, Family& F, const Level& L, const ConduitCoefs& cc, int newton, lpfem_ctx* c,
+                  const double* colscale) {
+  constexpr int WPB = D == 3 ? 16 : 8;  // 3D: 48 KB of tables + 16 x 10 KB of node buffers, one block per SM
+  constexpr size_t sm = cstep_smem<D, WPB>();
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_conduit_step_w<D, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  const dim3 grid((F.maxitems + WPB - 1) / WPB, (unsigned)F.hs.size());
+  k_conduit_step_w<D, WPB><<<grid, WPB * 32, sm, st>>>(F.ds, L, cc, newton, c->kmult, c->nc_p[0], c->nc_p[1], c->nc_p[2],
+                                                      refp<D>(c), F.rowptr, F.col, F.aconst, colscale, F.z, F.W, F.lag,
+                                                      F.qf, F.aux, F.aout, F.rhs);
   CKL();
 }
 
@@ -1272,11 +1321,7 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
   double hmin = 1e300;
   for (int a = 0; a < D; ++a) hmin = std::min(hmin, L.G.hc[a]);
   const ConduitCoefs cc = conduit_coefs<D>(c, c->cur_dt, hmin);
-  k_conduit_step_nb<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, L, cc, 1, c->kmult, c->nc_p[0], c->nc_p[1],
-                                                                c->nc_p[2], refp<D>(c), convtp<D>(c), F.rowptr, F.col,
-                                                                F.aconst, F.mask, F.z, F.W, F.lag, F.qf, F.aux, F.aout,
-                                                                F.rhs);
-  CKL();
+  conduit_step<D>(st, F, L, cc, 1, c, F.mask);
   const long long tot = c->haoff.back();
   CK(cudaMemsetAsync(c->abuf, 0, tot * sizeof(double), st));
   k_dense_batched<<<grid_rows(F.maxrows, ns), 128, 0, st>>>(F.ds, F.rowptr, F.col, F.aout, F.mask, c->daoff, c->abuf);
@@ -1318,9 +1363,11 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
   CKL();
 }
 
+// alg1: Algorithm 1 on T_h: every input (iterate, lagged velocity, p_F^n on Gamma) is a fine global array indexed
+// like the coarse Picard step (mode 2), so the system is the Newton-linearised fine implicit step about the iterate
 template <int D>
 void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, const double* cp_new,
-                        const double* cu_old, const double* cpF_old, double* out_u, double* out_p) {
+                        const double* cu_old, const double* cpF_old, double* out_u, double* out_p, bool alg1 = false) {
   Family& C = c->fam[lev][1];
   const int ns = (int)C.hs.size();
   if (!ns) return;
@@ -1342,6 +1389,16 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   A.porous_gamma_g = 2 * c->nc_p[D - 1] * A.R;
   A.mode = lev == 0 ? 2 : (c->opts.lag_mode == LPFEM_LAG_SUBDOMAIN ? 1 : 0);
   A.t = t;
+  if (alg1) {
+    A.mode = 2;
+    A.R = 1;
+    for (int a = 0; a < 3; ++a) {
+      A.nHc[a] = c->nf_c[a];
+      A.nHp[a] = c->nf_p[a];
+    }
+    A.n2_glob = c->n2c_f;
+    A.porous_gamma_g = 2 * c->nf_p[D - 1];
+  }
   k_conduit_prep<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(C.ds, c->Lc[lev], c->pd, c->co, A, C.base, C.z, C.W,
                                                                C.lag, C.qf, C.aux);
   CKL();
@@ -1356,10 +1413,7 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   }
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
-  k_conduit_step_nb<D><<<grid_rows(C.maxitems, ns), 128, 0, st>>>(
-      C.ds, c->Lc[lev], cc, newton, c->kmult, c->nc_p[0], c->nc_p[1], c->nc_p[2], refp<D>(c), convtp<D>(c), C.rowptr,
-      C.col, C.aconst, colscale, C.z, C.W, C.lag, C.qf, C.aux, C.aout, C.rhs);
-  CKL();
+  conduit_step<D>(st, C, c->Lc[lev], cc, newton, c, colscale);
   if (C.nbval) {
     k_nb_pack<D><<<grid_rows(C.maxitems * 32, ns), 128, 0, st>>>(C.ds, C.nbioff, C.rowptr, C.aout, C.nbvptr, C.nbval);
     CKL();
@@ -1525,6 +1579,75 @@ void halo_pack(lpfem_ctx* c);
 void halo_exchange_nccl(lpfem_ctx* c);
 void halo_unpack(lpfem_ctx* c);
 
+// coarse P2 node iH <- fine P2 node R gH (nested meshes): injection of D velocity components
+template <int D>
+__global__ void k_inject_p2(const double* __restrict__ fine, long long n2f, const int* npf, double* __restrict__ crs,
+                            long long n2c, int n0, int n1, int n2, int R) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n2c) return;
+  const int npc[3] = {2 * n0 + 1, 2 * n1 + 1, 2 * n2 + 1};
+  const int npff[3] = {2 * n0 * R + 1, 2 * n1 * R + 1, 2 * n2 * R + 1};
+  int g[3] = {0, 0, 0};
+  unlex<D>(i, npc, g);
+  for (int a = 0; a < D; ++a) g[a] *= R;
+  const long long gi = lex<D>(g, npff);
+  for (int a = 0; a < D; ++a) crs[a * n2c + i] = fine[a * n2f + gi];
+  (void)npf;
+}
+
+// Algorithm 1 on T_h at scale, with the batched multilevel Krylov kernels of the fine stage on whole-region
+// "subdomains" (grid 1, no overlap; H only sets the preconditioner hierarchy): the porous step (eqs. fullypF-
+// fullypm, lagged partners and the Gamma flux of u_h^n) by one preconditioned CG per field; the implicit
+// Navier-Stokes step (eq. fullyuc, p_F^n on Gamma) by Newton iterations from u_h^n, each a Newton-linearised Oseen
+// solve by preconditioned GMRES (the Algorithm 3 correction operator about the iterate), to the C11 test
+// ||du||_2 <= picard_rtol ||u||_2 -- the same discrete solution as Picard (oracle alg1.py).
+template <int D>
+void alg1_step(lpfem_ctx* c, double t) {
+  cudaStream_t st = c->st;
+  porous_stage<D>(c, 1, t, c->comp, c->comp, c->comp_u + (D - 1) * c->n2c_f, c->comp2, true);
+  const long long nu = (long long)D * c->n2c_f;
+  CK(cpya(c->a1u[0], c->comp_u, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cpya(c->a1p[0], c->comp_p, c->n1c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int cur = 0;
+  bool conv = false;
+  c->alg1_ok = true;
+  c->alg1_gm_ms = 0.0;
+  for (int it = 0; it < c->opts.picard_max && !conv; ++it) {
+    // preconditioner coarse boxes linearised at u_h^n, rebuilt every ml_refresh steps (as for Algorithm 3)
+    if (it == 0 && c->nl > 0 && (c->nstep - c->ml_built >= c->ml_refresh || c->ml_built < 0 || c->ml_dt != c->cur_dt)) {
+      k_inject_p2<D><<<(unsigned)((c->n2c_c + 255) / 256), 256, 0, st>>>(c->a1u[cur], c->n2c_f, nullptr, c->a1uH, c->n2c_c,
+                                                                         c->nc_c[0], c->nc_c[1], c->nc_c[2], c->R);
+      CKL();
+      coarse_box_inverses<D>(c, c->a1uH, c->ml_next);
+      c->ml_built = c->nstep;
+      c->ml_dt = c->cur_dt;
+    }
+    conduit_solve_once<D>(c, 1, t, c->a1u[cur], c->a1p[cur], c->comp_u, c->comp[2], c->a1u[1 - cur], c->a1p[1 - cur],
+                          true);
+    double dummy = 0;
+    bool ok = true;
+    fetch_stats(c, c->fam[1][1], 1, false, dummy, ok);
+    c->pending_res[1] = std::max(c->pending_res[1], dummy);
+    if (!ok) c->alg1_ok = false;
+    k_picard_norms<<<1, 1024, 0, st>>>(c->a1u[1 - cur], c->a1u[cur], nu, c->nrm);
+    CKL();
+    double hn[2];
+    CK(cpya(hn, c->nrm, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float mk = 0.0f;
+    CK(cudaEventElapsedTime(&mk, c->ek[2], c->ek[3]));
+    c->alg1_gm_ms += mk;
+    cur = 1 - cur;
+    c->stats.picard_iters++;
+    const double du = std::sqrt(hn[0]), un = std::sqrt(hn[1]);
+    if (!(du == du)) break;
+    conv = du <= c->opts.picard_rtol * un || du <= 1e-14 * std::sqrt((double)nu);
+  }
+  if (!conv) c->alg1_ok = false;
+  CK(cpya(c->comp2_u, c->a1u[cur], nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cpya(c->comp2_p, c->a1p[cur], c->n1c_f * sizeof(double), cudaMemcpyDeviceToDevice, st));
+}
+
 template <int D>
 void step_begin(lpfem_ctx* c, double dt) {
   CK(cudaSetDevice(c->dist.device));
@@ -1542,6 +1665,13 @@ void step_begin(lpfem_ctx* c, double dt) {
   const double t = time_at(c, n + 1, dt);  // C18
   c->pending_ok = true;
   c->pending_t = t;
+  c->pending_res[0] = c->pending_res[1] = 0.0;
+  if (c->alg1k) {  // Algorithm 1 on T_h: no coarse step, no local corrections
+    CK(cudaEventRecord(c->ev[1], st));
+    decide_fine_clusters<D>(c, false);
+    alg1_step<D>(c, t);
+    return;
+  }
   // ---------------- Step 1: coarse state n+1 (precomputed during the previous step when dt is unchanged; a
   // precomputed step that did not converge left coarse_n behind, so it is recomputed -- and reported -- here)
   if (c->coarse_n != n + 1 || c->coarse_dt != dt) {
@@ -1602,7 +1732,7 @@ void step_exchange(lpfem_ctx* c) {
 template <int D>
 void step_overlap(lpfem_ctx* c, double dt) {
   CK(cudaEventRecord(c->ev[2], c->st));
-  if (c->overlap && !c->kn.no_overlap) {
+  if (c->overlap && !c->kn.no_overlap && !c->alg1k) {
     try {
       coarse_step<D>(c, c->nstep + 1, dt);
     } catch (const Err& e) {
@@ -1617,7 +1747,11 @@ bool step_verdict(lpfem_ctx* c) {
   const bool alg1 = c->R == 1 && !c->kn.no_alg1_fastpath;
   double maxres[2] = {0, 0};
   bool ok = true;
-  if (!alg1) {
+  if (c->alg1k) {  // the conduit statistics were fetched per Newton iteration
+    fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
+    ok = ok && c->alg1_ok;
+    maxres[1] = c->pending_res[1];
+  } else if (!alg1) {
     fetch_stats(c, c->fam[1][0], 0, false, maxres[0], ok);
     fetch_stats(c, c->fam[1][1], 1, false, maxres[1], ok);
   } else {
@@ -1646,6 +1780,7 @@ void step_end(lpfem_ctx* c, bool ok_all) {
   CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
   if (!alg1 && !c->fam[1][0].hs.empty()) CK(cudaEventElapsedTime(&mk0, c->ek[0], c->ek[1]));
   if (!alg1 && !c->fam[1][1].hs.empty()) CK(cudaEventElapsedTime(&mk1, c->ek[2], c->ek[3]));
+  if (c->alg1k) mk1 = (float)c->alg1_gm_ms;
   c->stats.t_krylov_ms[0] += mk0;
   c->stats.t_krylov_ms[1] += mk1;
   c->stats.t_fine_ms += ms1;
@@ -1673,15 +1808,6 @@ void setup(lpfem_ctx* c) {
   build_ref<D>(*href);
   c->ref = dalloc<RefT<D>>(1);
   CK(cpy(c->ref, href, sizeof(RefT<D>), cudaMemcpyHostToDevice));
-  {
-    KuhnTables kt;
-    build_kuhn(D, kt);
-    ConvT<D>* hct = new ConvT<D>();
-    build_convt<D>(*href, kt, *hct);
-    c->convt = dalloc<ConvT<D>>(1);
-    CK(cpy(c->convt, hct, sizeof(ConvT<D>), cudaMemcpyHostToDevice));
-    delete hct;
-  }
   delete href;
   const lpfem_geometry& g = c->geom;
   const double steps[2] = {c->H, c->h};
@@ -1782,10 +1908,14 @@ void setup(lpfem_ctx* c) {
       Family& F = c->fam[lev][k];
       if (F.hs.empty()) continue;
       build_pattern<D>(c, F);
+      if (k == 1) check_row_len<D>(F);
       alloc_vectors(c, F);
       if (lev == 1) set_order(c, F, false);
-      // the fine conduit GMRES multiplies with a node-blocked copy of the operator (LPFEM_NO_NB: the CSR)
-      if (lev == 1 && k == 1 && !getenv("LPFEM_NO_NB")) build_nb<D>(c, F);
+      // the fine conduit GMRES multiplies with a node-blocked copy of the operator in 3D (cfg4 GMRES 1597 -> 1290 ms
+      // per step); 2D keeps the CSR (cfg2 144 -> 154 ms with it).  LPFEM_NB=0/1 forces either.
+      const char* nbk = getenv("LPFEM_NB");
+      const bool use_nb = nbk ? atoi(nbk) != 0 : (D == 3 && !getenv("LPFEM_NO_NB"));
+      if (lev == 1 && k == 1 && use_nb) build_nb<D>(c, F);
     }
   // multilevel preconditioner of the fine conduit systems: nested levels r h (r = 2, 4, .. dividing R)
   // and the coarse box at H (mlprec.cuh).  Requires the boxes to lie on coarse grid lines.
@@ -1850,6 +1980,7 @@ void setup(lpfem_ctx* c) {
         }
         finish_family(D, F);
         build_pattern<D>(c, F);
+        check_row_len<D>(F);
         alloc_vectors(c, F, true);
         c->ml.q[l] = l == 0 ? r : r / rs[l - 1];
         c->ml.r[l] = r;
@@ -2047,6 +2178,13 @@ void setup(lpfem_ctx* c) {
   c->comp_p = dalloc<double>(c->n1c_f);
   c->comp2_u = dalloc<double>(D * c->n2c_f);
   c->comp2_p = dalloc<double>(c->n1c_f);
+  if (c->alg1k) {
+    for (int k = 0; k < 2; ++k) {
+      c->a1u[k] = dalloc<double>(D * c->n2c_f);
+      c->a1p[k] = dalloc<double>(c->n1c_f);
+    }
+    c->a1uH = dalloc<double>(D * c->n2c_c);
+  }
   if (!c->hkmult.empty()) {
     c->kmult = dalloc<double>(c->hkmult.size());
     CK(cpy(c->kmult, c->hkmult.data(), c->hkmult.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -2073,7 +2211,14 @@ void setup(lpfem_ctx* c) {
     const int n = (int)c->fam[0][1].rows;
     if (cusolverDnCreate(&c->sol) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
     cusolverDnSetStream(c->sol, st);
-    CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    // the coarse step (one step ahead) runs at the highest stream priority: its small kernels are then dispatched
+    // ahead of the fine stage's waiting Krylov clusters instead of queueing behind them (the next fine step waits
+    // for it)
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    if (getenv("LPFEM_NO_PRIO")) prio_hi = prio_lo;
+    c->prio_hi = prio_hi;
+    CK(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi));
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
     {
@@ -2119,7 +2264,7 @@ void setup(lpfem_ctx* c) {
       c->linfo2 = dalloc<int>(1);
       c->nsi = nmax > c->kn.gj_max ? lpfem_ctx::NSI : 0;  // 3D boxes only (2D: batched Gauss-Jordan)
       for (int k = 0; k < c->nsi; ++k) {
-        CK(cudaStreamCreateWithFlags(&c->sinv[k], cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&c->sinv[k], cudaStreamNonBlocking, c->prio_hi));
         if (cusolverDnCreate(&c->hinv[k]) != CUSOLVER_STATUS_SUCCESS) throw Err(LPFEM_ECUDA, "cusolverDnCreate");
         cusolverDnSetStream(c->hinv[k], c->sinv[k]);
         c->lwki[k] = dalloc<double>(std::max(1, c->llwork));
@@ -2145,6 +2290,8 @@ void setup(lpfem_ctx* c) {
         A.comp[f] = c->comp[f];
       }
       A.coarse_u_old = c->cu[0];
+      for (int a = 0; a < 3; ++a) A.nHu[a] = c->nc_c[a];
+      A.Ru = c->R;
       for (int a = 0; a < 3; ++a) {
         A.nHp[a] = c->nc_p[a];
         A.nHc[a] = c->nc_c[a];
@@ -2529,6 +2676,14 @@ lpfem_status lpfem_create(const lpfem_geometry* geom, const lpfem_coeffs* coeffs
       throw Err(LPFEM_EINVAL, "gmres_restart: 0 (default) or the compiled restart length " + std::to_string(GM) +
                                   " (LPFEM_GM at build time)");
     c->opts.gmres_restart = GM;
+    if (c->opts.algorithm == 0) c->opts.algorithm = 3;
+    if (c->opts.algorithm != 1 && c->opts.algorithm != 3) throw Err(LPFEM_EINVAL, "algorithm: 1 or 3");
+    if (c->opts.algorithm == 1 && c->R > 1) {  // Algorithm 1 at scale: whole-region systems, H = preconditioner level
+      for (int a = 0; a < c->D; ++a)
+        if (c->m[a] != 1) throw Err(LPFEM_EINVAL, "algorithm 1: subdomain grid must be 1 (whole regions)");
+      if (c->ov != 0) throw Err(LPFEM_EINVAL, "algorithm 1: overlap must be 0");
+      c->alg1k = true;
+    }
     if (dist) {
       c->dist = *dist;
     } else {
@@ -3028,7 +3183,8 @@ void lpfem_destroy(lpfem_ctx* c) {
   for (int i = 0; i < 2; ++i)
     if (c->evcp[i]) cudaEventDestroy(c->evcp[i]);
   void* ptrs[] = {c->dense, c->dwork, c->piv, c->dinfo, c->wpic, c->wpic2, c->ppic, c->ppic2, c->nrm, c->comp[0], c->comp[1], c->comp[2], c->comp_u,
-                  c->comp_p, c->comp2[0], c->comp2[1], c->comp2[2], c->comp2_u, c->comp2_p, c->kmult, c->ref, c->convt};
+                  c->comp_p, c->comp2[0], c->comp2[1], c->comp2[2], c->comp2_u, c->comp2_p, c->kmult, c->ref,
+                  c->a1u[0], c->a1u[1], c->a1p[0], c->a1p[1], c->a1uH};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int i = 0; i < 4; ++i) {

@@ -150,29 +150,4 @@ void build_ref(RefT<D>& R) {
   }
 }
 
-// Convection tensors per simplex type on the unit cell (conduit.cuh ConvT): contractions of C3 with the
-// barycentric gradients of Kuhn simplex type t at h = 1.
-template <int D>
-void build_convt(const RefT<D>& R, const KuhnTables& K, ConvT<D>& C) {
-  std::memset(&C, 0, sizeof(C));
-  constexpr int N = n2_of(D), L = D + 1;
-  const double one[3] = {1.0, 1.0, 1.0};
-  for (int t = 0; t < nt_of(D); ++t) {
-    double G[D + 1][D];
-    kuhn_grad<D>(K.perm[t], one, G);
-    for (int i = 0; i < N; ++i)
-      for (int e = 0; e < D; ++e)
-        for (int j = 0; j < N; ++j)
-          for (int m = 0; m < N; ++m) {
-            double q = 0.0, tt = 0.0;
-            for (int k = 0; k < L; ++k) {
-              q += R.C3[i][m][j][k] * G[k][e];
-              tt += R.C3[i][j][m][k] * G[k][e];
-            }
-            C.Q[t][i][e][j][m] = q;
-            C.T[t][i][e][j][m] = tt;
-          }
-  }
-}
-
 }  // namespace lp

@@ -166,6 +166,33 @@ def test_dt_change_reassembles_and_converges():
     sim.close()
 
 
+@pytest.mark.parametrize("dim,h,H,problem,seed", [(2, 1 / 16, 1 / 4, "mms", None), (2, 1 / 16, 1 / 4, "injection", 2),
+                                                  (3, 1 / 8, 1 / 4, "mms", None), (3, 1 / 8, 1 / 4, "injection", 4)])
+def test_parity_algorithm1_at_scale_krylov(dim, h, H, problem, seed):
+    """SURVEY 8(f) rank 2 at scale: lpfem_opts.algorithm = 1 with H > h solves Algorithm 1 on T_h with
+    the fine stage's batched multilevel Krylov kernels on whole-region systems (grid 1, no overlap; H only sets the
+    preconditioner's coarsest level) and Newton iterations to the C11 test for the implicit Navier-Stokes step.
+    Parity against the oracle's Algorithm 1 (oracle/alg1.py: SuperLU, Picard) at the C20 bar, every step."""
+    from oracle import alg1
+    from oracle import mesh as M
+    from paper_2311_05170_b200 import LPFEM
+    dt = 0.1 if problem == "mms" else 0.01
+    cfg = I.make_config(dim=dim, H=H, h=h, grid=1, dt=dt, steps=3, problem=problem, seed=seed, overlap=0.0,
+                        algorithm=1)
+    Gp, Gc = M.region_grids(cfg, "h")
+    ora = alg1.Alg1(cfg, Gp, Gc, int(round(H / h)))
+    sim = LPFEM(cfg)
+    for n in range(cfg["steps"]):
+        ora.step()
+        sim.step()
+        o = {k: np.asarray(v) for k, v in ora.state.items()}
+        errs, bad = compare(sim.fields(), o)
+        assert not bad, f"step {n + 1}: {errs} {sim.stats()}"
+    st = sim.stats()
+    assert st["picard_iters"] >= cfg["steps"] and max(st["max_rel_residual"]) <= 1e-12
+    sim.close()
+
+
 @pytest.mark.parametrize("dim,h,dt", [(2, 1 / 16, 0.1), (3, 1 / 4, 0.1)])
 def test_parity_algorithm1_on_fine_mesh(dim, h, dt):
     """with H = h the library marches Algorithm 1 on T_h (the traditional
