@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rtol", type=float, default=None,
+                    help="override the Krylov relative residual (C19: 1e-12); comparison runs only")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--alg1", action="store_true",
                     help="Algorithm 1 on T_h (the traditional partitioned scheme, P:356-396) on the config's fine mesh, "
@@ -309,6 +311,9 @@ def main():
     if args.alg1:  # Algorithm 1 on T_h: whole regions (grid 1, no overlap), H = the preconditioner's coarsest level
         cfg = I.config(args.config, grid=1, overlap=0.0, algorithm=1)
         cfg["name"] += "-alg1"
+    if args.rtol is not None:
+        cfg["krylov_rtol"] = args.rtol
+        cfg["name"] += f"-rtol{args.rtol:g}"
     D = I.fine_dofs(cfg)
     stream = torch.cuda.Stream()
     nid = None

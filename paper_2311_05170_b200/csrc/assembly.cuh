@@ -363,6 +363,8 @@ struct PorousPrepArgs {
   int np_glob[3];                // P2 nodes per axis of the global fine porous region
   int conduit_gamma_g;           // conduit half-grid index of Gamma (0)
   int mode;                      // 0 composite (B), 1 subdomain (A), 2 coarse
+  int zero_base;                 // 1: base 0, the unknown is the full field (Algorithm 1 on T_h: no cancellation
+                                 //    in the right-hand side, so the C19 test is attainable)
   double t;                      // t_{n+1}
 };
 
@@ -389,7 +391,7 @@ __global__ void k_porous_prep(const SysDesc* __restrict__ sys, Level L, ProbData
     const long long k = f * rows_total + k0;
     double b, lg;
     if (A.mode == 2) {
-      b = A.coarse_new[f][lex<D>(g, A.np_glob)];
+      b = A.zero_base ? 0.0 : A.coarse_new[f][lex<D>(g, A.np_glob)];
       lg = A.coarse_old[f][lex<D>(g, A.np_glob)];
     } else {
       b = prolong_p2<D>(A.coarse_new[f], A.nHp, A.Rp, g);

@@ -174,6 +174,7 @@ struct ConduitPrepArgs {
   long long n2_glob;      // P2 nodes of the level's conduit region (component stride)
   int porous_gamma_g;     // half-grid index of Gamma in the porous region at the coarse level x R
   int mode;               // 0 fine composite (B), 1 fine subdomain (A), 2 coarse Picard, 3 operator only (U)
+  int zero_base;          // 1: base 0 (the unknown is the full field), wind = cu_new (Algorithm 1 on T_h)
   double t;
 };
 
@@ -221,8 +222,9 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
         if (A.mode == 0) lg = A.comp_u[a * A.n2_glob + lex<D>(g, A.np_glob)];
         else lg = prolong_p2<D>(A.cu_old + a * n2H, A.nHc, A.R, g) + A.ecorr[k];
       }
-      base[k] = b;
       W[k] = b;
+      if (A.zero_base) b = 0.0;
+      base[k] = b;
       z[k] = cls == CL_DIR ? gv[a] : b;
       lag[k] = lg;
       f[k] = fv[a];
@@ -251,6 +253,7 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
       b = prolong_p1<D>(A.cp_new, A.nHc, A.R, g);
     }
     const long long k = o + D * S.n2 + k1;
+    if (A.zero_base) b = 0.0;
     base[k] = b;
     z[k] = b;
   }
@@ -391,14 +394,10 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
     __syncwarp();
     // lane (j, e): se_e(j) = sum_m W_e(m) DA[p_e][i][m][j] / h_e; cv(j) = eta |K| sum_e se_e(j) (the D lanes of node j
     // exchange their terms, fixed order); the reaction of column block e from DB[p_e]
-    double ue[D][N];
+    // (the wind at the element nodes is read from shared memory: same address across the warp = broadcast)
     int sl[N];
 #pragma unroll
-    for (int m = 0; m < N; ++m) {
-      sl[m] = B.slot[m];
-#pragma unroll
-      for (int a = 0; a < D; ++a) ue[a][m] = B.Uw[a][sl[m]];
-    }
+    for (int m = 0; m < N; ++m) sl[m] = B.slot[m];
     const int j = act ? jl : 0;
     const int p = c_kt[D].pos[t][bl];
     const double* da = DA + ((p * N + i) * N) * N + j;
@@ -426,8 +425,9 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           double rv = 0.0;
+          const double* ua = B.Uw[a];
 #pragma unroll
-          for (int m = 0; m < N; ++m) rv += ue[a][m] * tv[m];
+          for (int m = 0; m < N; ++m) rv += ua[sl[m]] * tv[m];
           if (a == bl) self += sc * rv;
           else B.row[a][p0 + bl * Ln] += sc * rv;
         }

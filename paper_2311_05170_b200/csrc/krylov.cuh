@@ -408,32 +408,19 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
       const int L = ln.x, L1 = ln.y;
       if (node) {
         const int rl = D * L + L1;  // row length
-        // two neighbours per lane and round, loads unconditional (index clamped to the last neighbour, weight
-        // zeroed): 2 D^2 values, 2 columns and 2 D gathers in flight per lane
-        for (int k0 = lane; k0 < L; k0 += 2 * TPR) {
-          int kk[2], c[2];
-          double xb[2][D], vv[2][D][D];
+        for (int k = lane; k < L; k += TPR) {
+          const int c = __ldg(cl + k);
+          double xb[D], vv[D][D];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            kk[u] = min(k0 + u * TPR, L - 1);
-            c[u] = __ldg(cl + kk[u]);
+          for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int a = 0; a < D; ++a)
+            for (int bb = 0; bb < D; ++bb) vv[a][bb] = __ldg(v + a * rl + bb * L + k);
 #pragma unroll
-              for (int bb = 0; bb < D; ++bb) vv[u][a][bb] = __ldg(v + a * rl + bb * L + kk[u]);
-          }
+          for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
 #pragma unroll
-          for (int u = 0; u < 2; ++u)
+          for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int bb = 0; bb < D; ++bb) xb[u][bb] = x[bb * n2 + c[u]];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const double on = k0 + u * TPR < L ? 1.0 : 0.0;
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-              for (int bb = 0; bb < D; ++bb) acc[a] += (on * vv[u][a][bb]) * xb[u][bb];
-          }
+            for (int bb = 0; bb < D; ++bb) acc[a] += vv[a][bb] * xb[bb];
         }
         for (int k = lane; k < L1; k += TPR) {
           const int c = __ldg(cl + L + k);

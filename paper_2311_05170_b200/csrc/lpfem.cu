@@ -1056,11 +1056,15 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.p = C.W;
   a.V = C.V;
   a.rows_total = C.rows;
-  a.rtol = c->opts.krylov_rtol;
+  // Algorithm 1's Newton solves are in full-field form (zero base): the pressure's accuracy is the residual
+  // tolerance times the saddle point's conditioning, so they run to rtol / 10 (C19 still holds)
+  a.rtol = (C.level == 1 && c->alg1k) ? 0.1 * c->opts.krylov_rtol : c->opts.krylov_rtol;
   a.maxit = (C.level == 1 && c->fault_maxit[1] > 0) ? c->fault_maxit[1] : c->opts.max_iter;
   a.stat = C.dstat;
   a.q = C.q;
-  a.warm = (C.level == 1 && !c->kn.cold_start && !c->alg1k) ? std::min(C.solved, c->warm_order) : 0;
+  // Algorithm 1 on T_h: the unknown is the full field (zero base) and every Newton solve starts from the previous
+  // solution (the last iterate; at a step's first iteration u_h^n) without extrapolation
+  a.warm = (C.level == 1 && !c->kn.cold_start) ? (c->alg1k ? std::min(C.solved, 1) : std::min(C.solved, c->warm_order)) : 0;
   a.xp = a.warm > 0 ? C.xp : nullptr;
   a.order = C.level == 1 ? C.dorder : nullptr;
   if (C.nbval) {
@@ -1130,8 +1134,11 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
 
 // Cluster sizes of the fine Krylov launches, decided before the first fine stage: the conduit GMRES first (all its
 // clusters resident), then the porous PCG, which runs concurrently on st3, gets the SMs the conduit leaves free.
+// returns whether the porous and conduit stages run concurrently: not with conduit clusters of more than 8 CTAs
+// (cfg3: 16), whose placement the PCG's CTAs fragment so that a GMRES cluster waits for the PCG to end (measured
+// cfg3 GMRES 76 -> 105 ms concurrent)
 template <int D>
-void decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
+bool decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
   Family& C = c->fam[1][1];
   Family& P = c->fam[1][0];
   if (!C.hk.empty() && !C.cluster_checked && !C.bandwidth_bound) {
@@ -1149,11 +1156,13 @@ void decide_fine_clusters(lpfem_ctx* c, bool concurrent) {
       else chk(k_gmres<NTG, TPR3, GM, 3, false>);
     }
   }
+  concurrent = concurrent && C.cluster <= 8;
   if (concurrent && !P.hk.empty() && !P.cluster_checked && !P.bandwidth_bound && !C.hk.empty() &&
       !C.bandwidth_bound) {
     const int left = c->nsm - C.nsys_rule * C.cluster;
     P.cluster = std::max(1, std::min(P.cluster, left / P.nsys_rule));
   }
+  return concurrent;
 }
 
 // LPT launch order of a fine Krylov family: expected work rows x (iterations of the last solve + 1), largest first,
@@ -1256,6 +1265,7 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
   A.Ru = A.Rp;
   if (alg1) {
     A.mode = 2;
+    A.zero_base = 1;
     A.Rp = 1;
     A.Ru = 1;
     for (int a = 0; a < 3; ++a) A.nHu[a] = c->nf_c[a];
@@ -1391,6 +1401,7 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   A.t = t;
   if (alg1) {
     A.mode = 2;
+    A.zero_base = 1;
     A.R = 1;
     for (int a = 0; a < 3; ++a) {
       A.nHc[a] = c->nf_c[a];
@@ -1688,9 +1699,9 @@ void step_begin(lpfem_ctx* c, double dt) {
   // GMRES launch so that the GMRES clusters are placed first (ungated, the PCG fragmented the GPCs and a GMRES
   // cluster ran in a second wave).  Measured fine stage cfg0/1/2/3/4: 4.9/12.9/172/96/2327 ->
   // 4.5/11.4/150/91/2141 ms.  LPFEM_NO_CONCURRENT=1 serialises.
-  const bool conc = c->st3 && !c->kn.no_concurrent;
   const bool alg1 = c->R == 1 && !c->kn.no_alg1_fastpath;
-  if (!alg1) decide_fine_clusters<D>(c, conc);
+  bool conc = c->st3 && !c->kn.no_concurrent;
+  if (!alg1) conc = decide_fine_clusters<D>(c, conc);
   if (alg1) {
     // H = h: the coarse step is Algorithm 1 on T_h and every correction of Steps 3-4 vanishes
     // identically (the local problems' right-hand sides are the residuals of the converged coarse step in the

@@ -54,45 +54,73 @@ struct Stencil {
   double w[STMAX];
 };
 
+// Barycentric coordinates of a point in its coarse cell: numerators num[a] (over 2q) sorted descending by a
+// stable compare-exchange network (the Kuhn simplex containing the point, C22), with the axes they came from.
+// Written without runtime-indexed arrays so that everything stays in registers (the previous insertion sort
+// kept num/ord/V in local memory: ~600 local loads/stores in the 3D GMRES kernel).
+template <int D>
+__device__ __forceinline__ void kuhn_locate(const int g[3], int q, const int nc[3], int cell[3], long long lam[4],
+                                            int vcode[4]) {
+  int s0, s1 = 0, s2 = 0, o0 = 0, o1 = 1, o2 = 2;
+  int num[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    cell[a] = min(g[a] / (2 * q), nc[a] - 1);
+    num[a] = g[a] - 2 * q * cell[a];
+  }
+  s0 = num[0];
+  s1 = num[1];
+  s2 = num[2];
+  auto cx = [](int& va, int& oa, int& vb, int& ob) {  // descending, stable (strict comparison)
+    if (vb > va) {
+      const int tv = va, to = oa;
+      va = vb;
+      oa = ob;
+      vb = tv;
+      ob = to;
+    }
+  };
+  cx(s0, o0, s1, o1);
+  if (D > 2) {
+    cx(s1, o1, s2, o2);
+    cx(s0, o0, s1, o1);
+  }
+  auto p3 = [](int o) { return o == 0 ? 1 : (o == 1 ? 3 : 9); };
+  lam[0] = 2 * q - s0;
+  if (D == 2) {
+    lam[1] = s0 - s1;
+    lam[2] = s1;
+  } else {
+    lam[1] = s0 - s1;
+    lam[2] = s1 - s2;
+    lam[3] = s2;
+  }
+  vcode[0] = 0;
+  vcode[1] = 2 * p3(o0);
+  vcode[2] = vcode[1] + 2 * p3(o1);
+  if (D > 2) vcode[3] = vcode[2] + 2 * p3(o2);
+}
+
 // P2 prolongation weights of a point g (box-local half-grid of the finer level) in the coarser level box
 // (cells nc, ratio q): node codes within the coarse cell ({0,1,2}^D) and exact weights.
 template <int D>
 __device__ __forceinline__ void p2_weights(const int g[3], int q, const int nc[3], int cell[3], int code[n2_of(D)],
                                            double w[n2_of(D)]) {
-  int num[3], ord[3] = {0, 1, 2};
-  for (int a = 0; a < D; ++a) {
-    cell[a] = min(g[a] / (2 * q), nc[a] - 1);
-    num[a] = g[a] - 2 * q * cell[a];
-  }
-  for (int a = 1; a < D; ++a)
-    for (int b = a; b > 0 && num[ord[b]] > num[ord[b - 1]]; --b) {
-      int t = ord[b];
-      ord[b] = ord[b - 1];
-      ord[b - 1] = t;
-    }
   long long lam[4];
-  lam[0] = 2 * q - num[ord[0]];
-  for (int k = 1; k < D; ++k) lam[k] = num[ord[k - 1]] - num[ord[k]];
-  lam[D] = num[ord[D - 1]];
-  int V[4][3];
-  for (int a = 0; a < D; ++a) V[0][a] = 0;
-  for (int k = 1; k <= D; ++k) {
-    for (int a = 0; a < D; ++a) V[k][a] = V[k - 1][a];
-    V[k][ord[k - 1]] += 2;
-  }
+  int vc[4];
+  kuhn_locate<D>(g, q, nc, cell, lam, vc);
   const double inv = 1.0 / (2.0 * (double)q * (double)q);
   int n = 0;
+#pragma unroll
   for (int k = 0; k <= D; ++k, ++n) {
-    int c = 0, s = 1;
-    for (int a = 0; a < D; ++a, s *= 3) c += V[k][a] * s;
-    code[n] = c;
+    code[n] = vc[k];
     w[n] = (double)(lam[k] * (lam[k] - q)) * inv;
   }
+#pragma unroll
   for (int a = 0; a <= D; ++a)
+#pragma unroll
     for (int b = a + 1; b <= D; ++b, ++n) {
-      int c = 0, s = 1;
-      for (int e = 0; e < D; ++e, s *= 3) c += ((V[a][e] + V[b][e]) / 2) * s;
-      code[n] = c;
+      code[n] = (vc[a] + vc[b]) / 2;  // midpoint of vertices a, b (digits 0/2 -> 0/1/2)
       w[n] = (double)(2 * lam[a] * lam[b]) * inv;
     }
 }
@@ -100,28 +128,13 @@ __device__ __forceinline__ void p2_weights(const int g[3], int q, const int nc[3
 template <int D>
 __device__ __forceinline__ void p1_weights(const int g[3], int q, const int nc[3], int cell[3], int code[D + 1],
                                            double w[D + 1]) {
-  int num[3], ord[3] = {0, 1, 2};
-  for (int a = 0; a < D; ++a) {
-    cell[a] = min(g[a] / (2 * q), nc[a] - 1);
-    num[a] = g[a] - 2 * q * cell[a];
-  }
-  for (int a = 1; a < D; ++a)
-    for (int b = a; b > 0 && num[ord[b]] > num[ord[b - 1]]; --b) {
-      int t = ord[b];
-      ord[b] = ord[b - 1];
-      ord[b - 1] = t;
-    }
   long long lam[4];
-  lam[0] = 2 * q - num[ord[0]];
-  for (int k = 1; k < D; ++k) lam[k] = num[ord[k - 1]] - num[ord[k]];
-  lam[D] = num[ord[D - 1]];
-  int V[3] = {0, 0, 0};
+  int vc[4];
+  kuhn_locate<D>(g, q, nc, cell, lam, vc);
   const double inv = 1.0 / (2.0 * q);
+#pragma unroll
   for (int k = 0; k <= D; ++k) {
-    if (k > 0) V[ord[k - 1]] += 2;
-    int c = 0, s = 1;
-    for (int a = 0; a < D; ++a, s *= 3) c += V[a] * s;
-    code[k] = c;
+    code[k] = vc[k];
     w[k] = (double)lam[k] * inv;
   }
 }
