@@ -20,6 +20,7 @@ for n in range(k):
     print(f"step {n+1}: {time.time()-t:.3f}s coarse {s['t_coarse_ms']-prev['t_coarse_ms']:.1f}ms fine {s['t_fine_ms']-prev['t_fine_ms']:.1f}ms "
           f"pcg {s['t_krylov_ms'][0]-prev['t_krylov_ms'][0]:.1f}ms gmres {s['t_krylov_ms'][1]-prev['t_krylov_ms'][1]:.1f}ms "
           f"iters pcg sum {s['fine_iters'][0]-prev['fine_iters'][0]} max {s['fine_max_iters'][0]} gmres sum {s['fine_iters'][1]-prev['fine_iters'][1]} max {s['fine_max_iters'][1]} "
-          f"picard {s['picard_iters']-prev['picard_iters']} res {s['max_rel_residual']}", flush=True)
+          f"picard {s['picard_iters']-prev['picard_iters']} res {s['max_rel_residual']} "
+          f"bytes_krylov [{s['bytes_krylov'][0]-prev['bytes_krylov'][0]:.4e}, {s['bytes_krylov'][1]-prev['bytes_krylov'][1]:.4e}]", flush=True)
     prev = s
 print(json.dumps({k: v for k, v in s.items()}))
