@@ -25,6 +25,22 @@
 namespace lp {
 namespace cgx = cooperative_groups;
 
+// Matrix stream loads (values, column indices).  LPFEM_STREAM_LOADS=1 (experiment) uses the streaming cache hint
+// (ld.global.cs, evict-first) so that the matrix would not push the gathered vector x out of the L2 -- measured
+// much worse: the lanes of a row read the same 32-byte sectors at different times and evict-first re-fetched them
+// (cfg4 NB SpMV 13.5 -> 24.3 GB of DRAM traffic per product, GMRES 5.2 -> 8.9 TB per step)
+#ifndef LPFEM_STREAM_LOADS
+#define LPFEM_STREAM_LOADS 0
+#endif
+template <class T>
+__device__ __forceinline__ T ldm(const T* p) {
+#if LPFEM_STREAM_LOADS
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+
 struct KSys {
   long long row_off;   // vectors: first row of this system in the family's vector row space
   long long prow_off;  // pattern: first row of this system in rowptr
@@ -228,8 +244,8 @@ __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, cons
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const long long q = min(q0 + (long long)u * TPR, qe - 1);
-          cc[u] = __ldg(col + q);
-          vv[u] = __ldg(val + q);
+          cc[u] = ldm(col + q);
+          vv[u] = ldm(val + q);
         }
         // a warp barrier between the (col, val) loads and the x gathers keeps the compiler from interleaving
         // them (it otherwise schedules for 32 registers and chains col -> x per entry)
@@ -279,8 +295,8 @@ __device__ __forceinline__ void spmv_rows_pipe(const long long* __restrict__ rp,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long q = min(q0 + (long long)u * TPR, e - 1);
-        cc[u] = __ldg(col + q);
-        vv[u] = __ldg(val + q);
+        cc[u] = ldm(col + q);
+        vv[u] = ldm(val + q);
       }
     } else {
 #pragma unroll
@@ -359,7 +375,7 @@ __device__ __forceinline__ void spmv_rows_sm(const int* __restrict__ srp, const 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int q = min(q0 + u * TPR, qe - 1);  // unconditional loads (see spmv_rows)
-          vv[u] = __ldg(sval + q);
+          vv[u] = ldm(sval + q);
           xx[u] = x[scol[q]];
         }
 #pragma unroll
@@ -409,12 +425,12 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
       if (node) {
         const int rl = D * L + L1;  // row length
         for (int k = lane; k < L; k += TPR) {
-          const int c = __ldg(cl + k);
+          const int c = ldm(cl + k);
           double xb[D], vv[D][D];
 #pragma unroll
           for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int bb = 0; bb < D; ++bb) vv[a][bb] = __ldg(v + a * rl + bb * L + k);
+            for (int bb = 0; bb < D; ++bb) vv[a][bb] = ldm(v + a * rl + bb * L + k);
 #pragma unroll
           for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
 #pragma unroll
@@ -423,20 +439,20 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
             for (int bb = 0; bb < D; ++bb) acc[a] += vv[a][bb] * xb[bb];
         }
         for (int k = lane; k < L1; k += TPR) {
-          const int c = __ldg(cl + L + k);
+          const int c = ldm(cl + L + k);
           double vv[D];
 #pragma unroll
-          for (int a = 0; a < D; ++a) vv[a] = __ldg(v + a * rl + D * L + k);
+          for (int a = 0; a < D; ++a) vv[a] = ldm(v + a * rl + D * L + k);
           const double xp = x[D * n2 + c];
 #pragma unroll
           for (int a = 0; a < D; ++a) acc[a] += vv[a] * xp;
         }
       } else {
         for (int k = lane; k < L; k += TPR) {
-          const int c = __ldg(cl + k);
+          const int c = ldm(cl + k);
           double vv[D], xb[D];
 #pragma unroll
-          for (int bb = 0; bb < D; ++bb) vv[bb] = __ldg(v + bb * L + k);
+          for (int bb = 0; bb < D; ++bb) vv[bb] = ldm(v + bb * L + k);
 #pragma unroll
           for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
 #pragma unroll
