@@ -18,6 +18,7 @@
 //             ||b - A x||_2 <= rtol ||b||_2 (C19) is exact; every restart recomputes it.
 #pragma once
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "common.cuh"
 #include "mlprec.cuh"
@@ -29,6 +30,12 @@ namespace cgx = cooperative_groups;
 // (ld.global.cs, evict-first) so that the matrix would not push the gathered vector x out of the L2 -- measured
 // much worse: the lanes of a row read the same 32-byte sectors at different times and evict-first re-fetched them
 // (cfg4 NB SpMV 13.5 -> 24.3 GB of DRAM traffic per product, GMRES 5.2 -> 8.9 TB per step)
+#ifndef LPFEM_BASIS_F32
+#define LPFEM_BASIS_F32 1
+#endif
+#ifndef LPFEM_NB_COLFIRST
+#define LPFEM_NB_COLFIRST 0
+#endif
 #ifndef LPFEM_STREAM_LOADS
 #define LPFEM_STREAM_LOADS 0
 #endif
@@ -424,6 +431,32 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
       const int L = ln.x, L1 = ln.y;
       if (node) {
         const int rl = D * L + L1;  // row length
+#if LPFEM_NB_COLFIRST
+        // all of the lane's P2 columns first (one latency for the whole item instead of one per neighbour), then
+        // the gathers and values per neighbour
+        constexpr int KMAX = (72 + TPR - 1) / TPR;
+        int cc[KMAX];
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) cc[t] = lane + t * TPR < L ? ldm(cl + lane + t * TPR) : 0;
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) {
+          const int k = lane + t * TPR;
+          if (k < L) {
+            const int c = cc[t];
+            double xb[D], vv[D][D];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+              for (int bb = 0; bb < D; ++bb) vv[a][bb] = ldm(v + a * rl + bb * L + k);
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+              for (int bb = 0; bb < D; ++bb) acc[a] += vv[a][bb] * xb[bb];
+          }
+        }
+#else
         for (int k = lane; k < L; k += TPR) {
           const int c = ldm(cl + k);
           double xb[D], vv[D][D];
@@ -438,6 +471,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) acc[a] += vv[a][bb] * xb[bb];
         }
+#endif
         for (int k = lane; k < L1; k += TPR) {
           const int c = ldm(cl + L + k);
           double vv[D];
@@ -625,8 +659,8 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
 #endif
 constexpr int RLN = LPFEM_RLN;  // lanes per restricted row (4 vs 8: cfg2 GMRES 160 -> 153 ms, cfg1/cfg3 equal)
 
-template <int D, int NC>
-__device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ v, double* __restrict__ Z, int r0,
+template <int D, int NC, class VIN = double>
+__device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, double* __restrict__ Z, int r0,
                            int r1, int nrows) {
 #ifdef LPFEM_PHASE_TIMERS
   long long tsub = clock64();
@@ -678,13 +712,17 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     cl.sync();
   } else {
     SysDesc SF = S0;
-    const double* src = v;
+    const double* src = nullptr;  // the previous level (level 0 restricts the input v)
     for (int l = 0; l < P.nl; ++l) {
       const SysDesc SC = P.lsys[l][bx];
       double* dst = LRp(l);
       const int wfirst = (gt & ~31) / RLN;  // warp-uniform trip count (shuffles inside)
-      for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN)
-        restrict_item<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
+      for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN) {
+        if (l == 0)
+          restrict_item<D, NC, RLN>(SF, SC, P.st[l], v, dst, it, gt % RLN);
+        else
+          restrict_item<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
+      }
       SUBPHASE(2 * l);
       cl.sync();
       SUBPHASE(2 * l + 1);
@@ -752,7 +790,7 @@ __device__ void apply_prec(const MLArgs& P, int sid, const double* __restrict__ 
     const double si = s0[i];
     double zi = 0.0;
     if (si != 0.0) {
-      zi = si * v[i];
+      zi = si * (double)v[i];
       if (P.nl > 0) {
         if (P.direct == 1) {
           for (int l = 0; l < P.nl - 1; ++l)
@@ -901,9 +939,9 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
 // in chunks of 8 basis vectors (8 accumulators in registers; w is re-read once per chunk).  The 8 warp sums of
 // a chunk are formed by a reduce-scatter butterfly (xor 4, 2, 1: lane l keeps value l & 7) followed by two
 // shuffles across the lane octets: 9 shuffles per chunk instead of 8 x 5.  Fixed order: deterministic.
-template <int NT, int NV>
-__device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const double* __restrict__ Vt, long long ld,
-                                             const double* __restrict__ w, int nk, int k0, int r0, int r1) {
+template <int NT, int NV, class VT, class WT>
+__device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const VT* __restrict__ Vt, long long ld,
+                                             const WT* __restrict__ w, int nk, int k0, int r0, int r1) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const bool up4 = lane & 4, up2 = lane & 2, up1 = lane & 1;
@@ -911,11 +949,25 @@ __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const double* _
     double acc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-    for (int i = r0 + threadIdx.x; i < r1; i += NT) {
-      const double wi = w[i];
+    // two rows per round: 2 x 9 independent loads in flight per thread (the pass is latency-bound at one
+    // 1024-thread CTA per SM)
+    int i = r0 + threadIdx.x;
+    for (; i + NT < r1; i += 2 * NT) {
+      const double wa = (double)w[i], wb = (double)w[i + NT];
+      double va[8], vb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        va[u] = c0 + u < nk ? (double)Vt[(c0 + u) * ld + i] : 0.0;
+        vb[u] = c0 + u < nk ? (double)Vt[(c0 + u) * ld + i + NT] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += va[u] * wa + vb[u] * wb;
+    }
+    if (i < r1) {
+      const double wi = (double)w[i];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (c0 + u < nk) acc[u] += Vt[(c0 + u) * ld + i] * wi;
+        if (c0 + u < nk) acc[u] += (double)Vt[(c0 + u) * ld + i] * wi;
     }
     double a4[4], a2[2];
 #pragma unroll
@@ -937,18 +989,41 @@ __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const double* _
 
 // sum_{k<n} c[k] Vt_k[i], loads issued in batches of 8 independent basis reads (one L2/HBM latency per batch
 // instead of one per basis vector)
-__device__ __forceinline__ double basis_comb(const double* __restrict__ V, long long ld, const double* c, int n,
+template <class VT>
+__device__ __forceinline__ double basis_comb(const VT* __restrict__ V, long long ld, const double* c, int n,
                                              long long i) {
   double s = 0.0;
   for (int k0 = 0; k0 < n; k0 += 8) {
     double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = (k0 + u < n) ? V[(k0 + u) * ld + i] : 0.0;
+    for (int u = 0; u < 8; ++u) v[u] = (k0 + u < n) ? (double)V[(k0 + u) * ld + i] : 0.0;
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (k0 + u < n) s += c[k0 + u] * v[u];
   }
   return s;
+}
+
+// the same for rows i and i + NT at once (loads of both rows in flight together)
+template <int NT, class VT>
+__device__ __forceinline__ void basis_comb2(const VT* __restrict__ V, long long ld, const double* c, int n,
+                                            long long i, double& sa, double& sb) {
+  sa = 0.0;
+  sb = 0.0;
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    double va[8], vb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      va[u] = (k0 + u < n) ? (double)V[(k0 + u) * ld + i] : 0.0;
+      vb[u] = (k0 + u < n) ? (double)V[(k0 + u) * ld + i + NT] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < n) {
+        sa += c[k0 + u] * va[u];
+        sb += c[k0 + u] * vb[u];
+      }
+  }
 }
 
 // PC = false: right preconditioning folded into the matrix (A' = mask A diag(s)); the solution is y with
@@ -975,7 +1050,12 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   double* W = A.p + K.row_off;
   double* Zw = PC ? A.q + K.row_off : nullptr;
   const long long ld = A.rows_total;
-  double* V = A.V + K.row_off;
+  // Krylov basis: fp32 in the multilevel-preconditioned solves (PC), fp64 otherwise.  The basis is only the search
+  // space: the Arnoldi relation then holds to fp32 accuracy, which bounds the reduction a restart cycle can reach
+  // (~1e-7, against the ~1e-2..1e-3 the cycles achieve), and every restart recomputes the true residual in fp64,
+  // so the C19 test ||b - A x|| <= rtol ||b|| stays exact.  Halves the Gram-Schmidt traffic.
+  using VT = typename std::conditional<PC && LPFEM_BASIS_F32, float, double>::type;
+  VT* V = reinterpret_cast<VT*>(A.V) + K.row_off;
   // Hessenberg matrix in dynamic shared memory (static shared memory is capped at 48 KB), pattern after it
   extern __shared__ __align__(16) double lp_gdyn[];
   double(*H)[M] = reinterpret_cast<double(*)[M]>(lp_gdyn);
@@ -1042,7 +1122,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
     if (beta <= tol) conv = 1;
   }
   while (!conv) {
-    for (int i = r0 + tid; i < r1; i += NT) V[i] = r[i];
+    for (int i = r0 + tid; i < r1; i += NT) V[i] = (VT)r[i];
     if (tid == 0) {
       sig[0] = 1.0 / beta;
       gv[0] = beta;
@@ -1055,7 +1135,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       if (j == 0) cl.sync();
       PHASE(0);
       const double sj = sig[j];
-      if (PC) {
+      if constexpr (PC) {
         apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);
@@ -1079,15 +1159,25 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       __syncthreads();
       PHASE(3);
       // pass B: w' = w - sum_k h_k v_k, written as Vt_{j+1}; ||w'||^2
-      double* Vn = V + (j + 1) * ld;
+      VT* Vn = V + (j + 1) * ld;
       double pn = 0.0;
       if (tid <= j) hs[tid] = hc[tid] * sig[tid];
       __syncthreads();
-      for (int i = r0 + tid; i < r1; i += NT) {
-        double wi = W[i];
-        wi -= basis_comb(V, ld, hs, j + 1, i);
-        Vn[i] = wi;
-        pn += wi * wi;
+      {
+        int i = r0 + tid;
+        for (; i + NT < r1; i += 2 * NT) {  // two rows per round (loads in flight)
+          double ca, cb;
+          basis_comb2<NT>(V, ld, hs, j + 1, i, ca, cb);
+          const VT wa = (VT)(W[i] - ca), wb = (VT)(W[i + NT] - cb);
+          Vn[i] = wa;
+          Vn[i + NT] = wb;
+          pn += (double)wa * (double)wa + (double)wb * (double)wb;  // the norm of the stored vector
+        }
+        if (i < r1) {
+          const VT wv = (VT)(W[i] - basis_comb(V, ld, hs, j + 1, i));
+          Vn[i] = wv;
+          pn += (double)wv * (double)wv;
+        }
       }
       put_partial(S, 0, pn);
       cluster_sum(S, 1, par);
@@ -1102,9 +1192,11 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         if (tid <= j) hs[tid] = S.fin[tid] * sig[tid] * sig[tid];
         __syncthreads();
         for (int i = r0 + tid; i < r1; i += NT) {
-          double wi = Vn[i];
+          double wi = (double)Vn[i];
           wi -= basis_comb(V, ld, hs, j + 1, i);
-          Vn[i] = wi;
+          const VT wv = (VT)wi;
+          Vn[i] = wv;
+          wi = (double)wv;
           pn2 += wi * wi;
         }
         if (tid <= j) hc[tid] += S.fin[tid] * sig[tid];

@@ -1215,7 +1215,9 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
       } else {
         bytes += k.spmv * (12.0 * nz + 32.0 * rows);
       }
-      bytes += kind == 0 ? 64.0 * rows * k.iters : 48.0 * rows * k.iters + 16.0 * rows * k.vsum;
+      // (fp32 Krylov basis in the multilevel-preconditioned GMRES: 4 B per basis entry read or written)
+      const double vb = (kind == 1 && c->nl > 0 && F.level == 1 && LPFEM_BASIS_F32) ? 4.0 : 8.0;
+      bytes += kind == 0 ? 64.0 * rows * k.iters : (40.0 + vb) * rows * k.iters + 2.0 * vb * rows * k.vsum;
       // multilevel preconditioner, once per iteration: the fine vector read by the restriction and by the fine
       // combine, the fine scaling, the result (32 B/row); every level's restricted vector, scaling and correction
       // (~40 B per level row, the transfers' gathers hit the cache); the dense coarse-box inverse (fp32 conduit,

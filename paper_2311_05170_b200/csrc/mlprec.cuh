@@ -212,15 +212,15 @@ __global__ void k_set_identity_n(const SysDesc* __restrict__ sys, int nsub, cons
 // restriction by stencil gather.  Items are ordered class-major (component, parity class, node) so that
 // neighbouring items walk the same stencil; each item's stencil is split over LN lanes (lane = 0..LN-1 of an
 // aligned lane group) and reduced with shuffles, which cuts the dependent-load chain per row by LN.
-template <int D, int NC, int LN>
+template <int D, int NC, int LN, class ST>
 __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
-                                              const double* __restrict__ src, double* __restrict__ dst, int item,
+                                              const ST* __restrict__ src, double* __restrict__ dst, int item,
                                               int lane) {
   // every lane of the warp must reach the shuffles below: out-of-range items contribute nothing
   const bool valid = item < SC.nrows;
   if (!valid) item = 0;
   int l[3] = {0, 0, 0}, cls, row;
-  const double* sv;
+  const ST* sv;
   const int q = T->q;
   int shp[3];
   const int nvel = NC * SC.n2;
@@ -268,7 +268,7 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
       ok0 = ok0 && g0[a] >= 0 && g0[a] <= 2 * SF.nc[a];
       g0[a] = min(max(g0[a], 0), 2 * SF.nc[a]) >> sh;
     }
-    const double v = sv[lex<D>(g0, shp)];
+    const double v = (double)sv[lex<D>(g0, shp)];
     s0 += ok0 ? T->w[i] * v : 0.0;
   }
 #pragma unroll
