@@ -34,7 +34,7 @@ namespace cgx = cooperative_groups;
 #define LPFEM_BASIS_F32 1
 #endif
 #ifndef LPFEM_NB_COLFIRST
-#define LPFEM_NB_COLFIRST 0
+#define LPFEM_NB_COLFIRST 1
 #endif
 #ifndef LPFEM_STREAM_LOADS
 #define LPFEM_STREAM_LOADS 0
@@ -878,29 +878,59 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
     cl.sync();
     apply_prec<D, 1>(P, sid, r, z, r0, r1, K.nrows);
     double prz = 0.0;
-    for (int i = r0 + tid; i < r1; i += NT) prz += r[i] * z[i];
+    // vector passes two rows per round (independent loads of both rows in flight; the passes are latency-bound)
+    {
+      int i = r0 + tid;
+      for (; i + NT < r1; i += 2 * NT) prz += r[i] * z[i] + r[i + NT] * z[i + NT];
+      if (i < r1) prz += r[i] * z[i];
+    }
     put_partial(S, 0, prz);
     cluster_sum(S, 1, par);
     const double rzn = S.fin[0];
     const double beta = fresh ? 0.0 : rzn / rz;
     rz = rzn;
     fresh = false;
-    for (int i = r0 + tid; i < r1; i += NT) p[i] = z[i] + beta * p[i];
+    {
+      int i = r0 + tid;
+      for (; i + NT < r1; i += 2 * NT) {
+        const double za = z[i], zb = z[i + NT], pa = p[i], pb = p[i + NT];
+        p[i] = za + beta * pa;
+        p[i + NT] = zb + beta * pb;
+      }
+      if (i < r1) p[i] = z[i] + beta * p[i];
+    }
     cl.sync();
     spmv<NT, TPR>(PT, p, q, r0, r1);
     __syncthreads();
     double ppq = 0.0;
-    for (int i = r0 + tid; i < r1; i += NT) ppq += p[i] * q[i];
+    {
+      int i = r0 + tid;
+      for (; i + NT < r1; i += 2 * NT) ppq += p[i] * q[i] + p[i + NT] * q[i + NT];
+      if (i < r1) ppq += p[i] * q[i];
+    }
     put_partial(S, 0, ppq);
     cluster_sum(S, 1, par);
     const double pq = S.fin[0];
     const double alpha = pq != 0.0 ? rz / pq : 0.0;
     double prr = 0.0;
-    for (int i = r0 + tid; i < r1; i += NT) {
-      x[i] += alpha * p[i];
-      const double ri = r[i] - alpha * q[i];
-      r[i] = ri;
-      prr += w[i] * ri * ri;
+    {
+      int i = r0 + tid;
+      for (; i + NT < r1; i += 2 * NT) {
+        const double xa = x[i], xb = x[i + NT], pa = p[i], pb = p[i + NT];
+        const double ra0 = r[i], rb0 = r[i + NT], qa = q[i], qb = q[i + NT], wa = w[i], wb = w[i + NT];
+        x[i] = xa + alpha * pa;
+        x[i + NT] = xb + alpha * pb;
+        const double ra = ra0 - alpha * qa, rb = rb0 - alpha * qb;
+        r[i] = ra;
+        r[i + NT] = rb;
+        prr += wa * ra * ra + wb * rb * rb;
+      }
+      if (i < r1) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        prr += w[i] * ri * ri;
+      }
     }
     put_partial(S, 0, prr);
     cluster_sum(S, 1, par);
@@ -939,9 +969,11 @@ __global__ void __launch_bounds__(NT, 1) k_pcg_ml(KArgs A, MLArgs P, double* __r
 // in chunks of 8 basis vectors (8 accumulators in registers; w is re-read once per chunk).  The 8 warp sums of
 // a chunk are formed by a reduce-scatter butterfly (xor 4, 2, 1: lane l keeps value l & 7) followed by two
 // shuffles across the lane octets: 9 shuffles per chunk instead of 8 x 5.  Fixed order: deterministic.
+// ws: w is read as ws * w[i]; if pww != NULL the thread's sum of (ws w_i)^2 is added to *pww (first chunk)
 template <int NT, int NV, class VT, class WT>
 __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const VT* __restrict__ Vt, long long ld,
-                                             const WT* __restrict__ w, int nk, int k0, int r0, int r1) {
+                                             const WT* __restrict__ w, int nk, int k0, int r0, int r1,
+                                             double ws = 1.0, double* pww = nullptr) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const bool up4 = lane & 4, up2 = lane & 2, up1 = lane & 1;
@@ -951,9 +983,10 @@ __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const VT* __res
     for (int u = 0; u < 8; ++u) acc[u] = 0.0;
     // two rows per round: 2 x 9 independent loads in flight per thread (the pass is latency-bound at one
     // 1024-thread CTA per SM)
+    double ww = 0.0;
     int i = r0 + threadIdx.x;
     for (; i + NT < r1; i += 2 * NT) {
-      const double wa = (double)w[i], wb = (double)w[i + NT];
+      const double wa = ws * (double)w[i], wb = ws * (double)w[i + NT];
       double va[8], vb[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -962,13 +995,16 @@ __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const VT* __res
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc[u] += va[u] * wa + vb[u] * wb;
+      ww += wa * wa + wb * wb;
     }
     if (i < r1) {
-      const double wi = (double)w[i];
+      const double wi = ws * (double)w[i];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
         if (c0 + u < nk) acc[u] += (double)Vt[(c0 + u) * ld + i] * wi;
+      ww += wi * wi;
     }
+    if (pww && c0 == 0) *pww += ww;
     double a4[4], a2[2];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -1144,15 +1180,10 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         matvec(V + j * ld, W);
       }
       PHASE(2);
-      // w = sj * W;  pass A: h_k = sig_k Vt_k^T w and ||w||^2
+      // w = sj * W (applied on read, W is not rewritten);  pass A: h_k = sig_k Vt_k^T w and ||w||^2
       double pw = 0.0;
-      for (int i = r0 + tid; i < r1; i += NT) {
-        const double wi = sj * W[i];
-        W[i] = wi;
-        pw += wi * wi;
-      }
+      dots_chunked<NT, M + 2>(S, V, ld, W, j + 1, 0, r0, r1, sj, &pw);
       put_partial(S, j + 1, pw);
-      dots_chunked<NT, M + 2>(S, V, ld, W, j + 1, 0, r0, r1);
       cluster_sum(S, j + 2, par);
       if (tid <= j) hc[tid] = S.fin[tid] * sig[tid];
       const double ww = S.fin[j + 1];
@@ -1168,13 +1199,13 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         for (; i + NT < r1; i += 2 * NT) {  // two rows per round (loads in flight)
           double ca, cb;
           basis_comb2<NT>(V, ld, hs, j + 1, i, ca, cb);
-          const VT wa = (VT)(W[i] - ca), wb = (VT)(W[i + NT] - cb);
+          const VT wa = (VT)(sj * W[i] - ca), wb = (VT)(sj * W[i + NT] - cb);
           Vn[i] = wa;
           Vn[i + NT] = wb;
           pn += (double)wa * (double)wa + (double)wb * (double)wb;  // the norm of the stored vector
         }
         if (i < r1) {
-          const VT wv = (VT)(W[i] - basis_comb(V, ld, hs, j + 1, i));
+          const VT wv = (VT)(sj * W[i] - basis_comb(V, ld, hs, j + 1, i));
           Vn[i] = wv;
           pn += (double)wv * (double)wv;
         }

@@ -1217,7 +1217,9 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
       }
       // (fp32 Krylov basis in the multilevel-preconditioned GMRES: 4 B per basis entry read or written)
       const double vb = (kind == 1 && c->nl > 0 && F.level == 1 && LPFEM_BASIS_F32) ? 4.0 : 8.0;
-      bytes += kind == 0 ? 64.0 * rows * k.iters : (40.0 + vb) * rows * k.iters + 2.0 * vb * rows * k.vsum;
+      // GMRES per iteration: the product's output W written once and read by both Gram-Schmidt passes (24 B/row),
+      // the new basis vector written (vb), and the j+1 basis vectors read by each pass (2 vb per vector)
+      bytes += kind == 0 ? 64.0 * rows * k.iters : (24.0 + vb) * rows * k.iters + 2.0 * vb * rows * k.vsum;
       // multilevel preconditioner, once per iteration: the fine vector read by the restriction and by the fine
       // combine, the fine scaling, the result (32 B/row); every level's restricted vector, scaling and correction
       // (~40 B per level row, the transfers' gathers hit the cache); the dense coarse-box inverse (fp32 conduit,
@@ -1228,7 +1230,9 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
         double lrows = 0.0;
         for (int l = 0; l < nl; ++l) lrows += lv[l].hs[s].nrows;
         const double nL = lv[nl - 1].hs[s].nrows;
-        bytes += k.iters * (32.0 * rows + 40.0 * lrows + (kind == 0 ? 8.0 : 4.0) * nL * nL);
+        // (the fine vector read twice: 2 vb for the conduit's basis vector input, 16 for the porous residual)
+        const double fin = kind == 0 ? 32.0 : 16.0 + 2.0 * vb;
+        bytes += k.iters * (fin * rows + 40.0 * lrows + (kind == 0 ? 8.0 : 4.0) * nL * nL);
       }
     }
     c->stats.bytes_krylov[kind] += bytes;
