@@ -531,28 +531,43 @@ __global__ void k_nb_cols(const SysDesc* __restrict__ sys, const long long* __re
   for (int q = 0; q < ln.y; ++q) out[ln.x + q] = col[rb + D * ln.x + q] - D * S.n2;      // P1 vertices
 }
 
+// fp32 copy of an operator's values (grid-stride)
+__global__ void k_round_f32(const double* __restrict__ a, float* __restrict__ o, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    o[i] = (float)a[i];
+}
+
 // per step: the values of the item's row(s), in CSR order, into the node-blocked array (one warp per item,
 // coalesced copies)
 template <int D>
 __global__ void k_nb_pack(const SysDesc* __restrict__ sys, const long long* __restrict__ item_off,
                           const long long* __restrict__ rowptr, const double* __restrict__ aout,
-                          const long long* __restrict__ vptr, double* __restrict__ nbval) {
+                          const long long* __restrict__ vptr, double* __restrict__ nbval,
+                          float* __restrict__ nbval32) {
   const SysDesc S = sys[blockIdx.y];
   const int k = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (k >= S.n2 + S.n1) return;
   const long long g = item_off[blockIdx.y] + k;
   double* out = nbval + vptr[g];
+  float* out32 = nbval32 ? nbval32 + vptr[g] : nullptr;
+  auto put = [&](long long rb, long long re) {
+    for (long long q = rb + lane; q < re; q += 32) {
+      const double a = aout[q];
+      out[q - rb] = a;
+      if (out32) out32[q - rb] = (float)a;
+    }
+  };
   if (k < S.n2) {
     for (int a = 0; a < D; ++a) {
       const long long rb = rowptr[S.row_off + a * S.n2 + k], re = rowptr[S.row_off + a * S.n2 + k + 1];
-      for (long long q = rb + lane; q < re; q += 32) out[q - rb] = aout[q];
+      put(rb, re);
       out += re - rb;
+      if (out32) out32 += re - rb;
     }
   } else {
     const long long row = S.row_off + D * S.n2 + (k - S.n2);
-    const long long rb = rowptr[row], re = rowptr[row + 1];
-    for (long long q = rb + lane; q < re; q += 32) out[q - rb] = aout[q];
+    put(rowptr[row], rowptr[row + 1]);
   }
 }
 

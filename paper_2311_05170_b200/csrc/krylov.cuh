@@ -68,6 +68,7 @@ struct KSys {
 // stores 4 B per nonzero): 12 -> ~8.5 B per nonzero in 3D.
 struct NBMat {
   const double* val;
+  const float* val32;     // NULL, or the same values rounded to fp32 (the Arnoldi products of the multilevel GMRES)
   const int* col;
   const long long* vptr;  // per item (family item space): first value
   const long long* cptr;  // per item: first column
@@ -137,6 +138,7 @@ struct KArgs {
                      // 2: also xp holds the one before: initial guess 2 x - xp (linear extrapolation in time)
   double* xp;        // warm == 2: the solution two steps back (updated to the previous one)
   NBMat nb;          // GMRES: node-blocked operator (nb.val != NULL), else the CSR (rowptr, col, val)
+  const float* val32;  // GMRES (CSR): NULL, or the fp32 copy of val (same offsets) for the Arnoldi products
   const int* order;  // NULL, or the system of each cluster in launch order (clusters are dispatched in index
                      // order: the systems expected to take longest start first, LPT; no effect on the numbers)
 };
@@ -152,14 +154,16 @@ struct CtaPattern {
   const int* scol;      // shared: column indices of the CTA's nonzeros
   const double* sval;   // val + q0
   bool sm;
+  const float* val32;   // NULL, or the fp32 copy of val (the GMRES's Arnoldi products, 2D)
+  const float* sval32;  // val32 + q0
 };
 
 // dyn_off: bytes of dynamic shared memory in front of the pattern (the GMRES Hessenberg matrix)
 template <int NT>
 __device__ __forceinline__ CtaPattern stage_pattern(const KArgs& A, const long long* rp, const double* val, int r0,
-                                                    int r1, int dyn_off = 0) {
+                                                    int r1, int dyn_off = 0, const float* val32 = nullptr) {
   extern __shared__ __align__(16) int lp_ksm[];
-  CtaPattern P{rp, A.col, val, nullptr, nullptr, nullptr, A.smem_cols != 0};
+  CtaPattern P{rp, A.col, val, nullptr, nullptr, nullptr, A.smem_cols != 0, val32, nullptr};
   if (P.sm) {
     const long long q0 = rp[r0];
     const int nr = r1 - r0;
@@ -172,6 +176,7 @@ __device__ __forceinline__ CtaPattern stage_pattern(const KArgs& A, const long l
     P.srp = srp;
     P.scol = scol;
     P.sval = val + q0;
+    P.sval32 = val32 ? val32 + q0 : nullptr;
   }
   return P;
 }
@@ -229,9 +234,9 @@ __device__ __forceinline__ void put_partial(RedSmem<NT, NV>& S, int k, double v)
 // y[i] = sum_q val[q] x[col[q]] for rows [r0, r1), TPR lanes per row.  Each lane issues its (col, val) loads
 // in batches of U independent loads before the dependent x gathers, so that enough bytes are in flight per SM
 // to cover the HBM latency (Little's law: ~45 KB per SM at ~1 us).
-template <int NT, int TPR>
+template <int NT, int TPR, class MT = double>
 __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, const int* __restrict__ col,
-                                          const double* __restrict__ val, const double* __restrict__ x,
+                                          const MT* __restrict__ val, const double* __restrict__ x,
                                           double* __restrict__ y, int r0, int r1) {
   constexpr int U = 8;
   const int lane = threadIdx.x % TPR;
@@ -252,7 +257,7 @@ __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, cons
         for (int u = 0; u < U; ++u) {
           const long long q = min(q0 + (long long)u * TPR, qe - 1);
           cc[u] = ldm(col + q);
-          vv[u] = ldm(val + q);
+          vv[u] = (double)ldm(val + q);
         }
         // a warp barrier between the (col, val) loads and the x gathers keeps the compiler from interleaving
         // them (it otherwise schedules for 32 registers and chains col -> x per entry)
@@ -281,9 +286,9 @@ __device__ __forceinline__ void spmv_rows(const long long* __restrict__ rp, cons
 // Software-pipelined variant: while the x gathers of row r are in flight, the (col, val) batch of row r + NG and
 // the row pointers of row r + 2 NG are already loading (three stages), so the loads of a thread never wait on
 // one another; rows longer than TPR * U finish their extra batches inline.  Same sums as spmv_rows per batch.
-template <int NT, int TPR, int U>
+template <int NT, int TPR, int U, class MT = double>
 __device__ __forceinline__ void spmv_rows_pipe(const long long* __restrict__ rp, const int* __restrict__ col,
-                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               const MT* __restrict__ val, const double* __restrict__ x,
                                                double* __restrict__ y, int r0, int r1) {
   constexpr int NG = NT / TPR;
   const int lane = threadIdx.x % TPR;
@@ -297,7 +302,7 @@ __device__ __forceinline__ void spmv_rows_pipe(const long long* __restrict__ rp,
       e = 0;
     }
   };
-  auto load = [&](long long q0, long long e, int* cc, double* vv) {
+  auto load = [&](long long q0, long long e, int* cc, MT* vv) {
     if (q0 - lane < e) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -309,16 +314,16 @@ __device__ __forceinline__ void spmv_rows_pipe(const long long* __restrict__ rp,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         cc[u] = 0;
-        vv[u] = 0.0;
+        vv[u] = (MT)0;
       }
     }
   };
-  auto batch = [&](long long q0, long long e, const int* cc, double* vv) {
-    double xx[U];
+  auto batch = [&](long long q0, long long e, const int* cc, const MT* vm) {
+    double xx[U], vv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) xx[u] = x[cc[u]];
 #pragma unroll
-    for (int u = 0; u < U; ++u) vv[u] = q0 + (long long)u * TPR < e ? vv[u] * xx[u] : 0.0;
+    for (int u = 0; u < U; ++u) vv[u] = q0 + (long long)u * TPR < e ? (double)vm[u] * xx[u] : 0.0;
 #pragma unroll
     for (int w = U / 2; w > 0; w >>= 1)
 #pragma unroll
@@ -329,20 +334,20 @@ __device__ __forceinline__ void spmv_rows_pipe(const long long* __restrict__ rp,
   rowq(r, b0, e0);
   rowq(r + NG, b1, e1);
   int cc[U];
-  double vv[U];
+  MT vv[U];
   load(b0 + lane, e0, cc, vv);
   for (int base = r0; base < r1; base += NG) {
     long long b2, e2;
     rowq(r + 2 * NG, b2, e2);
     int cn[U];
-    double vn[U];
+    MT vn[U];
     load(b1 + lane, e1, cn, vn);
     double s = 0.0;
     if (b0 < e0) {
       s = batch(b0 + lane, e0, cc, vv);
       for (long long q0 = b0 + lane + (long long)TPR * U; q0 < e0; q0 += (long long)TPR * U) {
         int c2[U];
-        double v2[U];
+        MT v2[U];
         load(q0, e0, c2, v2);
         s += batch(q0, e0, c2, v2);
       }
@@ -364,9 +369,9 @@ __device__ __forceinline__ void spmv_rows_pipe(const long long* __restrict__ rp,
 }
 
 // same with the pattern staged in shared memory (row r of the system is srp[r - r0] .. srp[r - r0 + 1])
-template <int NT, int TPR>
+template <int NT, int TPR, class MT = double>
 __device__ __forceinline__ void spmv_rows_sm(const int* __restrict__ srp, const int* __restrict__ scol,
-                                             const double* __restrict__ sval, const double* __restrict__ x,
+                                             const MT* __restrict__ sval, const double* __restrict__ x,
                                              double* __restrict__ y, int r0, int r1) {
   constexpr int U = 8;
   const int lane = threadIdx.x % TPR;
@@ -382,7 +387,7 @@ __device__ __forceinline__ void spmv_rows_sm(const int* __restrict__ srp, const 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int q = min(q0 + u * TPR, qe - 1);  // unconditional loads (see spmv_rows)
-          vv[u] = ldm(sval + q);
+          vv[u] = (double)ldm(sval + q);
           xx[u] = x[scol[q]];
         }
 #pragma unroll
@@ -398,9 +403,19 @@ __device__ __forceinline__ void spmv_rows_sm(const int* __restrict__ srp, const 
 
 // PIPE: software-pipelined rows (measured better for the porous PCG and the 2D conduit GMRES: cfg4 PCG 321 -> 278
 // ms, cfg2 GMRES 167 -> 164 ms; worse for the 3D conduit GMRES: cfg3 99 -> 107 ms)
+// lowp: multiply with the fp32 copy of the values when the pattern carries one (the GMRES's Arnoldi products)
 template <int NT, int TPR, bool PIPE = true>
 __device__ __forceinline__ void spmv(const CtaPattern& P, const double* __restrict__ x, double* __restrict__ y, int r0,
-                                     int r1) {
+                                     int r1, bool lowp = false) {
+  if (lowp && P.val32) {
+    if (P.sm)
+      spmv_rows_sm<NT, TPR, float>(P.srp, P.scol, P.sval32, x, y, r0, r1);
+    else if (PIPE)
+      spmv_rows_pipe<NT, TPR, 4, float>(P.rp, P.col, P.val32, x, y, r0, r1);
+    else
+      spmv_rows<NT, TPR, float>(P.rp, P.col, P.val32, x, y, r0, r1);
+    return;
+  }
   if (P.sm)
     spmv_rows_sm<NT, TPR>(P.srp, P.scol, P.sval, x, y, r0, r1);
   else if (PIPE)
@@ -412,9 +427,9 @@ __device__ __forceinline__ void spmv(const CtaPattern& P, const double* __restri
 // y = A x over the items [i0, i1) of one system (node-blocked format), TPR lanes per item; y rows of node i are
 // a n2 + i, of vertex k: D n2 + k.  The lanes of an item walk its neighbours; per neighbour one column load, D
 // (node) x gathers and D^2 value loads, all independent.
-template <int NT, int TPR, int D>
-__device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int n2, const double* __restrict__ x,
-                                        double* __restrict__ y, int i0, int i1) {
+template <int NT, int TPR, int D, class MT = double>
+__device__ __forceinline__ void spmv_nb(const NBMat& B, const MT* __restrict__ vals, long long item_off, int n2,
+                                        const double* __restrict__ x, double* __restrict__ y, int i0, int i1) {
   constexpr int NG = NT / TPR;
   const int lane = threadIdx.x % TPR;
   for (int base = i0; base < i1; base += NG) {
@@ -426,7 +441,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
     if (it < i1) {
       const long long g = item_off + it;
       const int2 ln = B.len[g];
-      const double* v = B.val + B.vptr[g];
+      const MT* v = vals + B.vptr[g];
       const int* cl = B.col + B.cptr[g];
       const int L = ln.x, L1 = ln.y;
       if (node) {
@@ -447,7 +462,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
 #pragma unroll
             for (int a = 0; a < D; ++a)
 #pragma unroll
-              for (int bb = 0; bb < D; ++bb) vv[a][bb] = ldm(v + a * rl + bb * L + k);
+              for (int bb = 0; bb < D; ++bb) vv[a][bb] = (double)ldm(v + a * rl + bb * L + k);
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
 #pragma unroll
@@ -463,7 +478,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
 #pragma unroll
           for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int bb = 0; bb < D; ++bb) vv[a][bb] = ldm(v + a * rl + bb * L + k);
+            for (int bb = 0; bb < D; ++bb) vv[a][bb] = (double)ldm(v + a * rl + bb * L + k);
 #pragma unroll
           for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
 #pragma unroll
@@ -476,7 +491,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
           const int c = ldm(cl + L + k);
           double vv[D];
 #pragma unroll
-          for (int a = 0; a < D; ++a) vv[a] = ldm(v + a * rl + D * L + k);
+          for (int a = 0; a < D; ++a) vv[a] = (double)ldm(v + a * rl + D * L + k);
           const double xp = x[D * n2 + c];
 #pragma unroll
           for (int a = 0; a < D; ++a) acc[a] += vv[a] * xp;
@@ -486,7 +501,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
           const int c = ldm(cl + k);
           double vv[D], xb[D];
 #pragma unroll
-          for (int bb = 0; bb < D; ++bb) vv[bb] = ldm(v + bb * L + k);
+          for (int bb = 0; bb < D; ++bb) vv[bb] = (double)ldm(v + bb * L + k);
 #pragma unroll
           for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
 #pragma unroll
@@ -509,16 +524,16 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, long long item_off, int 
   }
 }
 
-// Standalone batched node-blocked SpMV over every system of the conduit family (lpfem_bench_spmv)
-template <int NT, int TPR, int D>
-__global__ void __launch_bounds__(NT) k_spmv_nb_family(const KSys* __restrict__ sys, NBMat B,
+// Standalone batched node-blocked SpMV over every system of the conduit family (lpfem_bench_spmv), fp64 or fp32 values
+template <int NT, int TPR, int D, class MT>
+__global__ void __launch_bounds__(NT) k_spmv_nb_family(const KSys* __restrict__ sys, NBMat B, const MT* vals,
                                                        const double* __restrict__ x, double* __restrict__ y,
                                                        int items_per_cta) {
   const KSys K = sys[blockIdx.y];
   const int i0 = blockIdx.x * items_per_cta;
   if (i0 >= K.n2 + K.n1) return;
   const int i1 = min(K.n2 + K.n1, i0 + items_per_cta);
-  spmv_nb<NT, TPR, D>(B, K.item_off, K.n2, x + K.row_off, y + K.row_off, i0, i1);
+  spmv_nb<NT, TPR, D, MT>(B, vals, K.item_off, K.n2, x + K.row_off, y + K.row_off, i0, i1);
 }
 
 // bytes of the GMRES(M) Hessenberg matrix (M + 1) x M in dynamic shared memory, 16-byte aligned
@@ -1095,18 +1110,24 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
   // Hessenberg matrix in dynamic shared memory (static shared memory is capped at 48 KB), pattern after it
   extern __shared__ __align__(16) double lp_gdyn[];
   double(*H)[M] = reinterpret_cast<double(*)[M]>(lp_gdyn);
-  const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1, gmres_h_bytes(M));
+  const CtaPattern PT = stage_pattern<NT>(A, rp, val, r0, r1, gmres_h_bytes(M), A.val32 ? A.val32 + K.val_off : nullptr);
   // node-blocked operator: the CTA's items (velocity nodes, then pressure vertices) instead of its rows; the
   // product then spans other CTAs' rows, so it ends with a cluster barrier
   const bool nbk = A.nb.val != nullptr;
   const int nitems = K.n2 + K.n1, ichunk = (nitems + CL - 1) / CL;
   const int it0 = min(nitems, crank * ichunk), it1 = min(nitems, it0 + ichunk);
-  auto matvec = [&](const double* X, double* Y) {
+  // lowp: the Arnoldi product of the multilevel GMRES multiplies with the fp32 copy of the operator when there is
+  // one (mixed-precision GMRES: the restart's true residual b - A x below is always the fp64 operator, so the
+  // C19 test stays exact; the fp32 operator only perturbs the search space, like the fp32 basis)
+  auto matvec = [&](const double* X, double* Y, bool lowp = false) {
     if (nbk) {
-      spmv_nb<NT, TPR, D>(A.nb, K.item_off, K.n2, X, Y, it0, it1);
+      if (lowp && A.nb.val32)
+        spmv_nb<NT, TPR, D, float>(A.nb, A.nb.val32, K.item_off, K.n2, X, Y, it0, it1);
+      else
+        spmv_nb<NT, TPR, D, double>(A.nb, A.nb.val, K.item_off, K.n2, X, Y, it0, it1);
       cl.sync();
     } else {
-      spmv<NT, TPR, D == 2>(PT, X, Y, r0, r1);
+      spmv<NT, TPR, D == 2>(PT, X, Y, r0, r1, lowp);
       __syncthreads();
     }
   };
@@ -1175,7 +1196,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
         apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);
-        matvec(Zw, W);
+        matvec(Zw, W, true);
       } else {
         matvec(V + j * ld, W);
       }

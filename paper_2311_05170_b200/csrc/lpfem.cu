@@ -170,6 +170,8 @@ struct Family {
   std::vector<KStat> hstat;
   // node-blocked copy of the fine conduit operator (krylov.cuh NBMat), used by the GMRES SpMV
   double* nbval = nullptr;
+  float* nbval32 = nullptr;      // fp32 copy for the Arnoldi products (mixed-precision GMRES), NULL with LPFEM_NB_F64
+  float* aout32 = nullptr;       // the same for the CSR operator of the fine conduit family without a node-blocked copy
   int* nbcol = nullptr;
   long long *nbvptr = nullptr, *nbcptr = nullptr, *nbioff = nullptr;
   int2* nblen = nullptr;
@@ -189,7 +191,7 @@ struct Family {
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
     void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, dinv, zv, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
-                    rhs, x, r, p, q, V, ecorr, ecorr2, dk, dstat, xp, dorder, nbval, nbcol, nbvptr, nbcptr,
+                    rhs, x, r, p, q, V, ecorr, ecorr2, dk, dstat, xp, dorder, nbval, nbval32, aout32, nbcol, nbvptr, nbcptr,
                     nbioff, nblen};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
@@ -505,6 +507,9 @@ void build_nb(lpfem_ctx* c, Family& F) {
   F.nb_ncols = tot[0];
   F.nbcol = dalloc<int>(F.nb_ncols);
   F.nbval = dalloc<double>(F.nnz);
+  // fp32 copy of the values for the GMRES's Arnoldi products (krylov.cuh k_gmres); LPFEM_NB_F64=1 (experiment)
+  // multiplies with the fp64 values throughout
+  if (!getenv("LPFEM_NB_F64")) F.nbval32 = dalloc<float>(F.nnz);
   k_nb_cols<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, F.nbioff, F.rowptr, F.col, F.nblen, F.nbcptr, F.nbcol);
   CKL();
 }
@@ -1050,6 +1055,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.rowptr = C.rowptr;
   a.col = C.col;
   a.val = C.aout;
+  a.val32 = C.aout32;
   a.b = C.rhs;
   a.x = C.x;
   a.r = C.r;
@@ -1068,7 +1074,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.xp = a.warm > 0 ? C.xp : nullptr;
   a.order = C.level == 1 ? C.dorder : nullptr;
   if (C.nbval) {
-    a.nb = NBMat{C.nbval, C.nbcol, C.nbvptr, C.nbcptr, C.nblen};
+    a.nb = NBMat{C.nbval, C.nbval32, C.nbcol, C.nbvptr, C.nbcptr, C.nblen};
   }
   C.solved = std::min(C.solved + 1, 2);
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
@@ -1211,9 +1217,14 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
       if (F.nbval) {
         const double items = F.hk[i].n2 + F.hk[i].n1;
         const double ncol = (double)F.nb_ncols * (nz / (double)F.nnz);  // the system's share of the columns
-        bytes += k.spmv * (8.0 * nz + 4.0 * ncol + 24.0 * items + 16.0 * rows);
+        // the Arnoldi products (one per iteration) read the fp32 values when there is an fp32 copy; the residual
+        // checks (warm start, every restart) the fp64 values
+        const double vbi = F.nbval32 ? 4.0 : 8.0;
+        bytes += k.iters * (vbi * nz + 4.0 * ncol + 24.0 * items + 16.0 * rows) +
+                 (k.spmv - k.iters) * (8.0 * nz + 4.0 * ncol + 24.0 * items + 16.0 * rows);
       } else {
-        bytes += k.spmv * (12.0 * nz + 32.0 * rows);
+        const double vbi = F.aout32 ? 8.0 : 12.0;  // (fp32 values in the Arnoldi products)
+        bytes += k.iters * (vbi * nz + 32.0 * rows) + (k.spmv - k.iters) * (12.0 * nz + 32.0 * rows);
       }
       // (fp32 Krylov basis in the multilevel-preconditioned GMRES: 4 B per basis entry read or written)
       const double vb = (kind == 1 && c->nl > 0 && F.level == 1 && LPFEM_BASIS_F32) ? 4.0 : 8.0;
@@ -1431,8 +1442,13 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
   conduit_step<D>(st, C, c->Lc[lev], cc, newton, c, colscale);
+  if (C.aout32) {
+    k_round_f32<<<(unsigned)std::min<long long>((C.nnz + 255) / 256, 148 * 16), 256, 0, st>>>(C.aout, C.aout32, C.nnz);
+    CKL();
+  }
   if (C.nbval) {
-    k_nb_pack<D><<<grid_rows(C.maxitems * 32, ns), 128, 0, st>>>(C.ds, C.nbioff, C.rowptr, C.aout, C.nbvptr, C.nbval);
+    k_nb_pack<D><<<grid_rows(C.maxitems * 32, ns), 128, 0, st>>>(C.ds, C.nbioff, C.rowptr, C.aout, C.nbvptr, C.nbval,
+                                                                  C.nbval32);
     CKL();
   }
   if (lev == 0) {
@@ -1933,6 +1949,8 @@ void setup(lpfem_ctx* c) {
       const char* nbk = getenv("LPFEM_NB");
       const bool use_nb = nbk ? atoi(nbk) != 0 : (D == 3 && !getenv("LPFEM_NO_NB"));
       if (lev == 1 && k == 1 && use_nb) build_nb<D>(c, F);
+      // 2D: an fp32 copy of the CSR values for the Arnoldi products of the multilevel GMRES (LPFEM_NB_F64=1: none)
+      if (lev == 1 && k == 1 && !use_nb && !getenv("LPFEM_NB_F64")) F.aout32 = dalloc<float>(F.nnz);
     }
   // multilevel preconditioner of the fine conduit systems: nested levels r h (r = 2, 4, .. dividing R)
   // and the coarse box at H (mlprec.cuh).  Requires the boxes to lie on coarse grid lines.
@@ -2988,14 +3006,15 @@ lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, dou
     constexpr int NT = 512;
     int tpr = family == 0 ? (c->D == 2 ? 4 : 8) : (c->D == 2 ? TPR2 : TPR3);
     if (family == 1 && F.nbval) {  // the node-blocked operator the GMRES multiplies with
-      const NBMat B{F.nbval, F.nbcol, F.nbvptr, F.nbcptr, F.nblen};
+      // the values the GMRES's Arnoldi products read: the fp32 copy when there is one
+      const NBMat B{F.nbval, F.nbval32, F.nbcol, F.nbvptr, F.nbcptr, F.nblen};
       int maxi = 0;
       double bytes = 0.0;
       for (size_t i = 0; i < F.hk.size(); ++i) {
         const KSys& K = F.hk[i];
         maxi = std::max(maxi, K.n2 + K.n1);
       }
-      bytes = 8.0 * F.nnz + 4.0 * F.nb_ncols + 24.0 * F.nb_items + 16.0 * F.rows;
+      bytes = (F.nbval32 ? 4.0 : 8.0) * F.nnz + 4.0 * F.nb_ncols + 24.0 * F.nb_items + 16.0 * F.rows;
       const int ipc = 4 * NT / tpr;
       const dim3 grid((maxi + ipc - 1) / ipc, (unsigned)F.hk.size());
       void* fb = nullptr;
@@ -3008,10 +3027,14 @@ lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, dou
       for (int r = 0; r < reps; ++r) {
         if (flush) CK(cudaMemsetAsync(fb, r & 0xff, fbytes, c->st));
         CK(cudaEventRecord(e0, c->st));
-        if (c->D == 2)
-          k_spmv_nb_family<NT, TPR2, 2><<<grid, NT, 0, c->st>>>(F.dk, B, F.rhs, F.W, ipc);
+        if (c->D == 2 && F.nbval32)
+          k_spmv_nb_family<NT, TPR2, 2, float><<<grid, NT, 0, c->st>>>(F.dk, B, F.nbval32, F.rhs, F.W, ipc);
+        else if (c->D == 2)
+          k_spmv_nb_family<NT, TPR2, 2, double><<<grid, NT, 0, c->st>>>(F.dk, B, F.nbval, F.rhs, F.W, ipc);
+        else if (F.nbval32)
+          k_spmv_nb_family<NT, TPR3, 3, float><<<grid, NT, 0, c->st>>>(F.dk, B, F.nbval32, F.rhs, F.W, ipc);
         else
-          k_spmv_nb_family<NT, TPR3, 3><<<grid, NT, 0, c->st>>>(F.dk, B, F.rhs, F.W, ipc);
+          k_spmv_nb_family<NT, TPR3, 3, double><<<grid, NT, 0, c->st>>>(F.dk, B, F.nbval, F.rhs, F.W, ipc);
         CKL();
         CK(cudaEventRecord(e1, c->st));
         CK(cudaEventSynchronize(e1));
