@@ -272,9 +272,14 @@ __global__ void k_conduit_prep(const SysDesc* __restrict__ sys, Level L, ProbDat
 //   rhs = mask * (b_load - A z), b_load = eta M f + (eta/dt) M u~^n [+ eta N(U) U] + Gamma loads.
 template <int D>
 struct CStepW;
+template <int D>
+constexpr int cstep_rel_bytes() {  // relative offset codes rel[t][i][m] (nt x N x N bytes), padded to 16 B
+  return (nt_of(D) * n2_of(D) * n2_of(D) + 15) & ~15;
+}
 template <int D, int WPB>
-constexpr size_t cstep_smem() {  // DA, DB (D x N^3 each), M22 (N^2), one CStepW per warp
-  return sizeof(double) * (2 * D * n2_of(D) * n2_of(D) * n2_of(D) + n2_of(D) * n2_of(D)) + WPB * sizeof(CStepW<D>);
+constexpr size_t cstep_smem() {  // DA, DB (D x N^3 each), M22 (N^2), rel codes, one CStepW per warp
+  return sizeof(double) * (2 * D * n2_of(D) * n2_of(D) * n2_of(D) + n2_of(D) * n2_of(D)) + cstep_rel_bytes<D>() +
+         WPB * sizeof(CStepW<D>);
 }
 template <int D>
 struct CStepW {
@@ -286,6 +291,8 @@ struct CStepW {
   double Lw[D][LMAX];   // eta f + (eta/dt) u~^n at the P2 neighbours
   int colr[RMAX];       // column list of the rows (block 0: P2 neighbours, ascending)
   int slot[N];          // position of the current simplex's nodes in the neighbour list
+  unsigned char map[D == 3 ? 128 : 32];  // slot of the P2 neighbour at half-grid offset d in [-2, 2]^D (code
+                                         // sum_a (d_a + 2) 5^a)
 };
 
 template <int D, int WPB>
@@ -303,11 +310,14 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
   // that the lanes (j, .) of a warp read consecutive words:
   //   DA[p][i][m][j] = C3[i][m][j][p+1] - C3[i][m][j][p]   (convection: phi_i phi_m d_c phi_j)
   //   DB[p][i][m][j] = C3[i][j][m][p+1] - C3[i][j][m][p]   (reaction:   phi_i phi_j d_c phi_m)
-  extern __shared__ __align__(16) double cstep_dyn[];  // DA, DB, M22, then one CStepW per warp (cstep_smem bytes)
+  extern __shared__ __align__(16) double cstep_dyn[];  // DA, DB, M22, rel, then one CStepW per warp (cstep_smem)
   double* DA = cstep_dyn;
   double* DB = cstep_dyn + NT3;
   double* sM = cstep_dyn + 2 * NT3;
-  CStepW<D>* wb = reinterpret_cast<CStepW<D>*>(cstep_dyn + 2 * NT3 + N * N);
+  // rel[t][i][m]: offset code of element node m relative to element node i in a simplex of type t (the same for
+  // every simplex of that type), so the slot of m in the neighbour list of the row node i is map[rel[t][i][m]]
+  unsigned char* rel = reinterpret_cast<unsigned char*>(cstep_dyn + 2 * NT3 + N * N);
+  CStepW<D>* wb = reinterpret_cast<CStepW<D>*>(reinterpret_cast<unsigned char*>(rel) + cstep_rel_bytes<D>());
   const SysDesc S = sys[blockIdx.y];
   const int nitems = S.n2 + S.n1;
   if ((int)(blockIdx.x * WPB) >= nitems) return;  // block-uniform
@@ -317,6 +327,12 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
     DB[k] = ref->C3[i][j][m][p + 1] - ref->C3[i][j][m][p];
   }
   for (int k = threadIdx.x; k < N * N; k += blockDim.x) sM[k] = (&ref->M22[0][0])[k];
+  for (int k = threadIdx.x; k < nt_of(D) * N * N; k += blockDim.x) {
+    const int m = k % N, i = (k / N) % N, t = k / (N * N);
+    int code = 0;
+    for (int a = 0, f = 1; a < D; ++a, f *= 5) code += (c_kt[D].off[t][m][a] - c_kt[D].off[t][i][a] + 2) * f;
+    rel[k] = (unsigned char)code;
+  }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * WPB + w;
@@ -369,6 +385,14 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
       B.Uw[a][q] = Ws[a * S.n2 + cq];
       B.Lw[a][q] = cc.eta * Fs[a * S.n2 + cq] + (cc.eta / cc.dt) * Ls[a * S.n2 + cq];
     }
+  // slot map of the P2 neighbours (every element node of a simplex at the node is one of them)
+  for (int q = lane; q < Ln; q += 32) {
+    int v[3] = {0, 0, 0};
+    unlex<D>(B.colr[q], S.np, v);
+    int code = 0;
+    for (int a = 0, f = 1; a < D; ++a, f *= 5) code += (v[a] - l[a] + 2) * f;
+    B.map[code] = (unsigned char)q;
+  }
   const double vol = kuhn_volume<D>(L.G.hc);
   const double ev = cc.eta * vol;
   double ih[D];
@@ -380,17 +404,7 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
   double bpart = 0.0;
   __syncwarp();
   for_simplices_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
-    if (lane < N) {  // slot of element node m in the neighbour list (binary search in shared memory)
-      int v[3];
-      for (int a = 0; a < D; ++a) v[a] = 2 * c[a] + c_kt[D].off[t][lane][a];
-      const int key = (int)lex<D>(v, S.np);
-      int lo = 0, hi = Ln;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (B.colr[mid] < key) lo = mid + 1; else hi = mid;
-      }
-      B.slot[lane] = lo;
-    }
+    if (lane < N) B.slot[lane] = B.map[rel[(t * N + i) * N + lane]];  // slot of element node m = lane
     __syncwarp();
     // lane (j, e): se_e(j) = sum_m W_e(m) DA[p_e][i][m][j] / h_e; cv(j) = eta |K| sum_e se_e(j) (the D lanes of node j
     // exchange their terms, fixed order); the reaction of column block e from DB[p_e]
