@@ -10,6 +10,7 @@
 // r+1 / r, here r = 1: Taylor-Hood P2-P1 and P2 pressures (BASELINE configs).
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cmath>
 
 #define HD __host__ __device__ __forceinline__

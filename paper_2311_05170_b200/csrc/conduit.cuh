@@ -276,10 +276,18 @@ template <int D>
 constexpr int cstep_rel_bytes() {  // relative offset codes rel[t][i][m] (nt x N x N bytes), padded to 16 B
   return (nt_of(D) * n2_of(D) * n2_of(D) + 15) & ~15;
 }
+template <int D>
+constexpr int cstep_cl_bytes() {  // simplex lists per parity class: (1 << D) x 8 nt shorts, then (1 << D) counts
+  return (((1 << D) * 8 * nt_of(D) * 2 + (1 << D) * 4) + 15) & ~15;
+}
+template <int D>
+constexpr int cstep_tab_bytes() {  // DA, DB (D x N^3 each), M22 (N^2), rel codes, simplex lists: 16-byte multiple
+  return (int)sizeof(double) * (2 * D * n2_of(D) * n2_of(D) * n2_of(D) + n2_of(D) * n2_of(D)) + cstep_rel_bytes<D>() +
+         cstep_cl_bytes<D>();
+}
 template <int D, int WPB>
-constexpr size_t cstep_smem() {  // DA, DB (D x N^3 each), M22 (N^2), rel codes, one CStepW per warp
-  return sizeof(double) * (2 * D * n2_of(D) * n2_of(D) * n2_of(D) + n2_of(D) * n2_of(D)) + cstep_rel_bytes<D>() +
-         WPB * sizeof(CStepW<D>);
+constexpr size_t cstep_smem() {  // the tables, then one CStepW per warp
+  return cstep_tab_bytes<D>() + WPB * sizeof(CStepW<D>);
 }
 template <int D>
 struct CStepW {
@@ -291,9 +299,71 @@ struct CStepW {
   double Lw[D][LMAX];   // eta f + (eta/dt) u~^n at the P2 neighbours
   int colr[RMAX];       // column list of the rows (block 0: P2 neighbours, ascending)
   int slot[N];          // position of the current simplex's nodes in the neighbour list
+  double Ue[D * N];     // wind at the current simplex's nodes, component-major (Ue[a N + m])
   unsigned char map[D == 3 ? 128 : 32];  // slot of the P2 neighbour at half-grid offset d in [-2, 2]^D (code
                                          // sum_a (d_a + 2) 5^a)
 };
+
+
+// the reference tables of k_conduit_step_w (one CTA, once per context): built in shared memory with the kernel's
+// layout, then stored to tab (cstep_tab_bytes<D>() bytes) for the per-CTA copies
+template <int D>
+__global__ void k_cstep_tables(const RefT<D>* __restrict__ ref, double* __restrict__ tab) {
+  constexpr int N = n2_of(D);
+  constexpr int NT3 = D * N * N * N;
+  extern __shared__ __align__(16) double cstep_dyn[];
+  double* DA = cstep_dyn;
+  double* DB = cstep_dyn + NT3;
+  double* sM = cstep_dyn + 2 * NT3;
+  unsigned char* rel = reinterpret_cast<unsigned char*>(cstep_dyn + 2 * NT3 + N * N);
+  short(*s_cl)[8 * nt_of(D)] = reinterpret_cast<short(*)[8 * nt_of(D)]>(rel + cstep_rel_bytes<D>());
+  int* s_ncl = reinterpret_cast<int*>(rel + cstep_rel_bytes<D>() + (1 << D) * 8 * nt_of(D) * 2);
+  for (int k = threadIdx.x; k < NT3; k += blockDim.x) {
+    const int j = k % N, m = (k / N) % N, i = (k / (N * N)) % N, p = k / (N * N * N);
+    DA[k] = ref->C3[i][m][j][p + 1] - ref->C3[i][m][j][p];
+    DB[k] = ref->C3[i][j][m][p + 1] - ref->C3[i][j][m][p];
+  }
+  for (int k = threadIdx.x; k < N * N; k += blockDim.x) sM[k] = (&ref->M22[0][0])[k];
+  // simplex lists per parity class of a node (for_simplices_at's enumeration with the cube candidates of an interior
+  // node: per even axis the cubes l/2 - 1 and l/2, per odd axis (l - 1)/2)
+    if (threadIdx.x < (1 << D)) {
+    const int pcl = threadIdx.x;
+    int n = 0;
+    const int n2 = D > 2 ? ((pcl >> 2) & 1 ? 1 : 2) : 1, n1 = D > 1 ? ((pcl >> 1) & 1 ? 1 : 2) : 1;
+    const int n0 = (pcl & 1) ? 1 : 2;
+    for (int i2 = 0; i2 < n2; ++i2)
+      for (int i1 = 0; i1 < n1; ++i1)
+        for (int i0 = 0; i0 < n0; ++i0) {
+          const int ii[3] = {i0, i1, i2};
+          int code = 0, f = 1, dcm = 0;
+          for (int a = 0; a < D; ++a, f *= 3) {
+            int o;  // offset of the node in the cube (half-grid units)
+            if ((pcl >> a) & 1) {
+              o = 1;
+            } else if (ii[a] == 0) {
+              o = 2;  // cube l/2 - 1
+              dcm |= 1 << a;
+            } else {
+              o = 0;  // cube l/2
+            }
+            code += o * f;
+          }
+          for (int t = 0; t < nt_of(D); ++t) {
+            const int i = c_kt[D].lookup[t][code];
+            if (i >= 0) s_cl[pcl][n++] = (short)(dcm | (t << 3) | (i << 6));
+          }
+        }
+    s_ncl[pcl] = n;
+  }
+  for (int k = threadIdx.x; k < nt_of(D) * N * N; k += blockDim.x) {
+    const int m = k % N, i = (k / N) % N, t = k / (N * N);
+    int code = 0;
+    for (int a = 0, f = 1; a < D; ++a, f *= 5) code += (c_kt[D].off[t][m][a] - c_kt[D].off[t][i][a] + 2) * f;
+    rel[k] = (unsigned char)code;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < cstep_tab_bytes<D>() / 8; k += blockDim.x) tab[k] = cstep_dyn[k];
+}
 
 template <int D, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
@@ -302,7 +372,8 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
                  const long long* __restrict__ rowptr, const int* __restrict__ col,
                  const double* __restrict__ aconst, const double* __restrict__ s, const double* __restrict__ z,
                  const double* __restrict__ W, const double* __restrict__ lag, const double* __restrict__ f,
-                 const double* __restrict__ pfg, double* __restrict__ aout, double* __restrict__ rhs) {
+                 const double* __restrict__ pfg, double* __restrict__ aout, double* __restrict__ rhs, int nbx,
+                 int nsys, int* __restrict__ ticket, const double* __restrict__ tab) {
   constexpr int N = n2_of(D);
   constexpr int NT3 = D * N * N * N;
   // barycentric-gradient differences of C3 (gradients of Kuhn simplices are +-1/h: sum_k C3[..][k] G[k][c] =
@@ -317,26 +388,38 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
   // rel[t][i][m]: offset code of element node m relative to element node i in a simplex of type t (the same for
   // every simplex of that type), so the slot of m in the neighbour list of the row node i is map[rel[t][i][m]]
   unsigned char* rel = reinterpret_cast<unsigned char*>(cstep_dyn + 2 * NT3 + N * N);
-  CStepW<D>* wb = reinterpret_cast<CStepW<D>*>(reinterpret_cast<unsigned char*>(rel) + cstep_rel_bytes<D>());
-  const SysDesc S = sys[blockIdx.y];
-  const int nitems = S.n2 + S.n1;
-  if ((int)(blockIdx.x * WPB) >= nitems) return;  // block-uniform
-  for (int k = threadIdx.x; k < NT3; k += blockDim.x) {
-    const int j = k % N, m = (k / N) % N, i = (k / (N * N)) % N, p = k / (N * N * N);
-    DA[k] = ref->C3[i][m][j][p + 1] - ref->C3[i][m][j][p];
-    DB[k] = ref->C3[i][j][m][p + 1] - ref->C3[i][j][m][p];
+  const short(*s_cl)[8 * nt_of(D)] = reinterpret_cast<const short(*)[8 * nt_of(D)]>(rel + cstep_rel_bytes<D>());
+  const int* s_ncl = reinterpret_cast<const int*>(rel + cstep_rel_bytes<D>() + (1 << D) * 8 * nt_of(D) * 2);
+  CStepW<D>* wb = reinterpret_cast<CStepW<D>*>(reinterpret_cast<unsigned char*>(cstep_dyn) + cstep_tab_bytes<D>());
+  // persistent CTAs: the tables are built once per CTA, then the CTA walks blocks of WPB nodes (one warp per node)
+  // of the virtual grid (nbx node blocks x nsys systems) with a stride of gridDim.x, or, with a ticket counter
+  // (zeroed before the launch), takes the next block in order (the blocks in flight then stay a compact window of
+  // the node order: cfg4 DRAM reads 33 -> 15 GB per launch, but the block barrier per step made it slower, 51.7 ->
+  // 57.0 ms; the fine family uses the stride).  A grid of one CTA per block makes it the plain one-shot kernel.
+  __shared__ int s_next;
+  auto grab = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) s_next = (int)gridDim.x + atomicAdd(ticket, 1);
+    __syncthreads();
+    return s_next;
+  };
+  if ((long long)gridDim.x >= (long long)nbx * nsys) {  // one CTA per block: an empty block exits before the copy
+    const SysDesc S0 = sys[blockIdx.x / nbx];
+    if ((int)(blockIdx.x % nbx) * WPB >= S0.n2 + S0.n1) return;
   }
-  for (int k = threadIdx.x; k < N * N; k += blockDim.x) sM[k] = (&ref->M22[0][0])[k];
-  for (int k = threadIdx.x; k < nt_of(D) * N * N; k += blockDim.x) {
-    const int m = k % N, i = (k / N) % N, t = k / (N * N);
-    int code = 0;
-    for (int a = 0, f = 1; a < D; ++a, f *= 5) code += (c_kt[D].off[t][m][a] - c_kt[D].off[t][i][a] + 2) * f;
-    rel[k] = (unsigned char)code;
+  {  // the tables (built once by k_cstep_tables), copied with 16-byte loads
+    const int4* src = reinterpret_cast<const int4*>(tab);
+    int4* dst = reinterpret_cast<int4*>(cstep_dyn);
+    for (int k = threadIdx.x; k < cstep_tab_bytes<D>() / 16; k += blockDim.x) dst[k] = __ldg(src + k);
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * WPB + w;
-  if (r >= nitems) return;
+  for (int vb = blockIdx.x; vb < nbx * nsys; vb = ticket ? grab() : vb + (int)gridDim.x) {
+  const SysDesc S = sys[vb / nbx];
+  const int nitems = S.n2 + S.n1;
+  const int r = (vb % nbx) * WPB + w;
+  if (r >= nitems) continue;
+  __syncwarp();
   const long long o = S.row_off;
   const double* zs = z + o;
   const double* ss = s + o;
@@ -354,7 +437,7 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) b += __shfl_xor_sync(0xffffffffu, b, k);
     if (lane == 0) rhs[row] = fixed ? 0.0 : b;
-    return;
+    continue;
   }
   CStepW<D>& B = wb[w];
   const int nHp[3] = {nHp0, nHp1, nHp2};
@@ -395,33 +478,34 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
   }
   const double vol = kuhn_volume<D>(L.G.hc);
   const double ev = cc.eta * vol;
-  double ih[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) ih[a] = 1.0 / L.G.hc[a];
   // lane (j, bb): element node j, column block bb (also the component whose right-hand side it accumulates)
   const int jl = lane / D, bl = lane % D;
+  const double ihb = 1.0 / L.G.hc[bl], scb = ev / L.G.hc[bl];  // per lane, once
   const bool act = lane < N * D;
   double bpart = 0.0;
   __syncwarp();
-  for_simplices_at<D>(l, S.nc, [&](const int c[3], int t, int i) {
-    if (lane < N) B.slot[lane] = B.map[rel[(t * N + i) * N + lane]];  // slot of element node m = lane
+  auto simplex = [&](int t, int i) {
+    // lane k < D N: slot of element node m = k mod N and the wind component k / N there (one gather per lane;
+    // afterwards every lane reads the element's wind at fixed offsets, a broadcast)
+    if (act) {
+      const int m = lane % N;
+      const int sm = B.map[rel[(t * N + i) * N + m]];
+      if (lane < N) B.slot[m] = sm;
+      B.Ue[lane] = B.Uw[lane / N][sm];
+    }
     __syncwarp();
     // lane (j, e): se_e(j) = sum_m W_e(m) DA[p_e][i][m][j] / h_e; cv(j) = eta |K| sum_e se_e(j) (the D lanes of node j
     // exchange their terms, fixed order); the reaction of column block e from DB[p_e]
-    // (the wind at the element nodes is read from shared memory: same address across the warp = broadcast)
-    int sl[N];
-#pragma unroll
-    for (int m = 0; m < N; ++m) sl[m] = B.slot[m];
     const int j = act ? jl : 0;
     const int p = c_kt[D].pos[t][bl];
     const double* da = DA + ((p * N + i) * N) * N + j;
     const double* db = DB + ((p * N + i) * N) * N + j;
     double se = 0.0;
     if (act) {
-      const double* ub = B.Uw[bl];
+      const double* ub = B.Ue + bl * N;
 #pragma unroll
-      for (int m = 0; m < N; ++m) se += ub[sl[m]] * da[m * N];
-      se *= 1.0 / L.G.hc[bl];
+      for (int m = 0; m < N; ++m) se += ub[m] * da[m * N];
+      se *= ihb;
     }
     double cv = 0.0;
 #pragma unroll
@@ -435,13 +519,13 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
         double tv[N];
 #pragma unroll
         for (int m = 0; m < N; ++m) tv[m] = db[m * N];
-        const double sc = ev / L.G.hc[bl];
+        const double sc = scb;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           double rv = 0.0;
-          const double* ua = B.Uw[a];
+          const double* ua = B.Ue + a * N;
 #pragma unroll
-          for (int m = 0; m < N; ++m) rv += ua[sl[m]] * tv[m];
+          for (int m = 0; m < N; ++m) rv += ua[m] * tv[m];
           if (a == bl) self += sc * rv;
           else B.row[a][p0 + bl * Ln] += sc * rv;
         }
@@ -451,7 +535,25 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
       bpart += vol * sM[i * N + j] * B.Lw[bl][p0];
     }
     __syncwarp();
-  });
+  };
+  // the simplices at the node, in for_simplices_at's order, from the list of its parity class: entry = (cube
+  // offsets dc_a in {-1, 0} of the even axes (bit a set: -1), type t, local index i); a cube outside the box is
+  // skipped (uniform across the warp)
+  {
+    const int pcl = parity_class<D>(l);
+    const int ne = s_ncl[pcl];
+    for (int e = 0; e < ne; ++e) {
+      const int code = s_cl[pcl][e];
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        if (!(l[a] & 1)) {
+          const int ca = (l[a] >> 1) - ((code >> a) & 1);
+          ok = ok && ca >= 0 && ca < S.nc[a];
+        }
+      if (ok) simplex((code >> 3) & 7, code >> 6);
+    }
+  }
   // right-hand side per component: lanes with bl == a hold its partial sums (fixed-order shuffle tree)
   double bsum[D];
 #pragma unroll
@@ -500,6 +602,7 @@ k_conduit_step_w(const SysDesc* __restrict__ sys, Level L, ConduitCoefs cc, int 
     for (int k = 16; k > 0; k >>= 1) bz += __shfl_xor_sync(0xffffffffu, bz, k);
     if (lane == 0) rhs[o + a * S.n2 + r] = fixed ? 0.0 : bsum[a] - bz;
   }
+  }  // virtual blocks
 }
 
 // ---- node-blocked copy of a conduit family's CSR operator (krylov.cuh NBMat); item g = item_off + k of system s
@@ -543,6 +646,29 @@ __global__ void k_nb_cols(const SysDesc* __restrict__ sys, const long long* __re
   const long long rb = rowptr[row];
   for (int q = 0; q < ln.x; ++q) out[q] = col[rb + q];                                   // P2 nodes (< n2)
   for (int q = 0; q < ln.y; ++q) out[ln.x + q] = col[rb + D * ln.x + q] - D * S.n2;      // P1 vertices
+}
+
+// 16-bit column offsets of the node-blocked operator: per item the bases (first P2 column, first P1 column; the
+// blocks are sorted ascending) and column - base; *bad set when an offset does not fit 16 bits
+template <int D>
+__global__ void k_nb_cols16(const SysDesc* __restrict__ sys, const long long* __restrict__ item_off,
+                            const int2* __restrict__ len, const long long* __restrict__ cptr,
+                            const int* __restrict__ nbcol, unsigned short* __restrict__ col16,
+                            int2* __restrict__ cbase, int* __restrict__ bad) {
+  const SysDesc S = sys[blockIdx.y];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= S.n2 + S.n1) return;
+  const long long g = item_off[blockIdx.y] + k;
+  const int2 ln = len[g];
+  const int* in = nbcol + cptr[g];
+  const int b2 = ln.x > 0 ? in[0] : 0, b1 = ln.y > 0 ? in[ln.x] : 0;
+  cbase[g] = make_int2(b2, b1);
+  unsigned short* out = col16 + cptr[g];
+  for (int q = 0; q < ln.x + ln.y; ++q) {
+    const int off = in[q] - (q < ln.x ? b2 : b1);
+    if (off < 0 || off > 65535) *bad = 1;
+    out[q] = (unsigned short)off;
+  }
 }
 
 // fp32 copy of an operator's values (grid-stride)

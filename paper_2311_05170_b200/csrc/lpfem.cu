@@ -172,7 +172,11 @@ struct Family {
   double* nbval = nullptr;
   float* nbval32 = nullptr;      // fp32 copy for the Arnoldi products (mixed-precision GMRES), NULL with LPFEM_NB_F64
   float* aout32 = nullptr;       // the same for the CSR operator of the fine conduit family without a node-blocked copy
+  float* val32 = nullptr;        // fine porous family: fp32 copy of the 3 operators (mixed-precision PCG)
+  int* ticket = nullptr;         // block counter of the persistent conduit assembly (k_conduit_step_w)
   int* nbcol = nullptr;
+  unsigned short* nbcol16 = nullptr;  // 16-bit column offsets (experiment LPFEM_NB_COL16; NULL by default)
+  int2* nbcbase = nullptr;
   long long *nbvptr = nullptr, *nbcptr = nullptr, *nbioff = nullptr;
   int2* nblen = nullptr;
   long long nb_items = 0, nb_ncols = 0;
@@ -191,7 +195,7 @@ struct Family {
   std::vector<std::array<int, 3>> core0, core1;
   void free_all() {
     void* ptrs[] = {ds, rowptr, col, val, diag, isq, wn, dinv, zv, aconst, aout, scale, mask, base, z, lag, qf, aux, W,
-                    rhs, x, r, p, q, V, ecorr, ecorr2, dk, dstat, xp, dorder, nbval, nbval32, aout32, nbcol, nbvptr, nbcptr,
+                    rhs, x, r, p, q, V, ecorr, ecorr2, dk, dstat, xp, dorder, nbval, nbval32, aout32, val32, ticket, nbcol, nbcol16, nbcbase, nbvptr, nbcptr,
                     nbioff, nblen};
     for (void* ptr : ptrs)
       if (ptr) cudaFree(ptr);
@@ -222,6 +226,9 @@ struct lpfem_ctx {
   int nsm = 148;               // SMs of the device
   cudaStream_t st3 = nullptr;  // fine porous stage, concurrent with the fine conduit stage (independent)
   cudaEvent_t evp[3] = {};     // fork / join of st3; [2]: conduit GMRES about to launch (gates the porous PCG)
+  cudaStream_t st4 = nullptr;  // split GMRES launch (experiment LPFEM_GM_SPLIT): the light systems' launch
+  cudaEvent_t evs[2] = {};     // fork / join of st4
+  int gm_split[3] = {0, 0, 0}; // LPFEM_GM_SPLIT=k:c_heavy:c_light (heaviest k systems by expected work)
   bool gate = false;           // concurrent fine stage: record / wait evp[2] around the Krylov launches
   cudaEvent_t evc[3] = {};
   cudaEvent_t evcp[2] = {};  // coarse step parts: after the porous solves, after the Navier-Stokes iteration
@@ -276,6 +283,8 @@ struct lpfem_ctx {
   MLArgs ml{};
   double *part = nullptr, *aci = nullptr, *abuf = nullptr, *lwk = nullptr;
   float* ainv[2] = {nullptr, nullptr};   // row-major coarse-box inverses (fp32), double-buffered (coarse_box_inverses)
+  __nv_bfloat16* ainvb[2] = {nullptr, nullptr};  // experiment LPFEM_ML_BF16: the same in bf16
+  double* cstab = nullptr;               // reference tables of the conduit assembly (k_cstep_tables)
   int ml_next = 0, ml_busy = 0;          // slot the next fine step uses / slot the enqueued fine step reads
   int warm_order = 2;                    // Krylov initial guess: 1 previous solution, 2 linear extrapolation
   // experiment switches (environment, read once at create)
@@ -284,6 +293,7 @@ struct lpfem_ctx {
     bool no_concurrent = false, no_alg1_fastpath = false, no_overlap = false;
     double reorth2 = 0.1;
     int gj_max = 512;
+    double pcg_rr_fac = 1e-10;  // mixed-precision PCG: true-residual replacement when ||r||^2 fell by this factor
   } kn;
   // coarse Navier-Stokes chord iteration: LU of the last factorised Jacobian in `dense`/`piv` (conduit_solve_once)
   bool clu_valid = false, clu_force = false;
@@ -512,6 +522,29 @@ void build_nb(lpfem_ctx* c, Family& F) {
   if (!getenv("LPFEM_NB_F64")) F.nbval32 = dalloc<float>(F.nnz);
   k_nb_cols<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, F.nbioff, F.rowptr, F.col, F.nblen, F.nbcptr, F.nbcol);
   CKL();
+  // 16-bit column offsets (2 instead of 4 B per (item, neighbour)): a column lies within a few grid planes of the
+  // item's first column in a box's lexicographic numbering.  Experiment (LPFEM_NB_COL16=1): measured slower (cfg4
+  // standalone SpMV 2.07 -> 2.47 ms, GMRES 747 -> 839 ms per step: the per-item base load and the adds sit in the
+  // dependent column -> gather chain), so the 32-bit columns stay the default
+  if (getenv("LPFEM_NB_COL16")) {
+    F.nbcol16 = dalloc<unsigned short>(F.nb_ncols);
+    F.nbcbase = dalloc<int2>(ni);
+    int* dbad = dalloc<int>(1);
+    CK(cudaMemsetAsync(dbad, 0, sizeof(int), st));
+    k_nb_cols16<D><<<grid_rows(F.maxitems, ns), 128, 0, st>>>(F.ds, F.nbioff, F.nblen, F.nbcptr, F.nbcol, F.nbcol16,
+                                                              F.nbcbase, dbad);
+    CKL();
+    int bad = 0;
+    CK(cpya(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(dbad);
+    if (bad) {
+      cudaFree(F.nbcol16);
+      cudaFree(F.nbcbase);
+      F.nbcol16 = nullptr;
+      F.nbcbase = nullptr;
+    }
+  }
 }
 
 // the warp-per-node conduit assembly keeps a node's rows in shared memory (CStepW<D>::RMAX entries per row)
@@ -987,6 +1020,11 @@ void assemble_dt(lpfem_ctx* c, double dt) {
       k_porous_scale<D><<<grid_rows(P.maxrows, ns), 128, 0, st>>>(P.ds, P.rowptr, P.col, P.val, P.nnz, P.isq,
                                                                    P.rows);
       CKL();
+      if (P.val32) {
+        k_round_f32<<<(unsigned)std::min<long long>((3 * P.nnz + 255) / 256, 148 * 16), 256, 0, st>>>(P.val, P.val32,
+                                                                                                     3 * P.nnz);
+        CKL();
+      }
     }
     conduit_const<D>(c, c->fam[lev][1], c->Lc[lev], dt);
   }
@@ -1002,6 +1040,8 @@ void solve_porous(lpfem_ctx* c, Family& P) {
   a.rowptr = P.rowptr;
   a.col = P.col;
   a.val = P.val;
+  a.val32 = P.val32;
+  a.rr_fac = c->kn.pcg_rr_fac;
   a.b = P.rhs;
   a.w = P.wn;
   a.x = P.x;
@@ -1074,7 +1114,7 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
   a.xp = a.warm > 0 ? C.xp : nullptr;
   a.order = C.level == 1 ? C.dorder : nullptr;
   if (C.nbval) {
-    a.nb = NBMat{C.nbval, C.nbval32, C.nbcol, C.nbvptr, C.nbcptr, C.nblen};
+    a.nb = NBMat{C.nbval, C.nbval32, C.nbcol, C.nbvptr, C.nbcptr, C.nblen, nullptr, nullptr};
   }
   C.solved = std::min(C.solved + 1, 2);
   // reorthogonalise only on severe cancellation (||w'|| < 0.316 ||w||); measured: the Kahan-Parlett 1/sqrt(2)
@@ -1098,7 +1138,22 @@ void solve_conduit(lpfem_ctx* c, Family& C) {
     }
     const size_t sm = pattern_smem(k, C, C.cluster, hb, c->kn.no_smem_pattern || C.nbval);
     a.smem_cols = sm > 0;
-    launch_cluster_sm(k, (int)C.hk.size(), C.cluster, NTG, hb + sm, c->st, a, c->ml);
+    const int nsys = (int)C.hk.size();
+    if (c->st4 && C.level == 1 && C.nbval && a.order && c->gm_split[0] < nsys) {
+      // experiment: the heaviest systems (launch order = expected work) in one launch with larger clusters, the
+      // rest beside it on st4 with smaller ones, so that all clusters fit one wave
+      const int kh = c->gm_split[0];
+      KArgs al = a;
+      al.order = a.order + kh;
+      CK(cudaEventRecord(c->evs[0], c->st));
+      CK(cudaStreamWaitEvent(c->st4, c->evs[0], 0));
+      launch_cluster_sm(k, kh, c->gm_split[1], NTG, hb, c->st, a, c->ml);
+      launch_cluster_sm(k, nsys - kh, c->gm_split[2], NTG, hb, c->st4, al, c->ml);
+      CK(cudaEventRecord(c->evs[1], c->st4));
+      CK(cudaStreamWaitEvent(c->st, c->evs[1], 0));
+      return;
+    }
+    launch_cluster_sm(k, nsys, C.cluster, NTG, hb + sm, c->st, a, c->ml);
   };
   if (pc) {
     if (D == 2)
@@ -1220,10 +1275,12 @@ void fetch_stats(lpfem_ctx* c, Family& F, int kind, bool coarse, double& maxres,
         // the Arnoldi products (one per iteration) read the fp32 values when there is an fp32 copy; the residual
         // checks (warm start, every restart) the fp64 values
         const double vbi = F.nbval32 ? 4.0 : 8.0;
-        bytes += k.iters * (vbi * nz + 4.0 * ncol + 24.0 * items + 16.0 * rows) +
-                 (k.spmv - k.iters) * (8.0 * nz + 4.0 * ncol + 24.0 * items + 16.0 * rows);
+        // (columns: 2 B offsets + 8 B of bases per item with the 16-bit columns, else 4 B)
+        const double cb = F.nbcol16 ? 2.0 * ncol + 8.0 * items : 4.0 * ncol;
+        bytes += k.iters * (vbi * nz + cb + 24.0 * items + 16.0 * rows) +
+                 (k.spmv - k.iters) * (8.0 * nz + cb + 24.0 * items + 16.0 * rows);
       } else {
-        const double vbi = F.aout32 ? 8.0 : 12.0;  // (fp32 values in the Arnoldi products)
+        const double vbi = (F.aout32 || F.val32) ? 8.0 : 12.0;  // (fp32 values in the Arnoldi / CG products)
         bytes += k.iters * (vbi * nz + 32.0 * rows) + (k.spmv - k.iters) * (12.0 * nz + 32.0 * rows);
       }
       // (fp32 Krylov basis in the multilevel-preconditioned GMRES: 4 B per basis entry read or written)
@@ -1308,7 +1365,7 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
 // per-step conduit operator and right-hand side of a family (conduit.cuh k_conduit_step_w: one warp per node / row)
 template <int D>
 void conduit_step(cudaStream_t st, Family& F, const Level& L, const ConduitCoefs& cc, int newton, lpfem_ctx* c,
-                  const double* colscale) {
+                  const double* colscale, bool fine_main = false) {
   constexpr int WPB = D == 3 ? 16 : 8;  // 3D: 48 KB of tables + 16 x 10 KB of node buffers, one block per SM
   constexpr size_t sm = cstep_smem<D, WPB>();
   static bool attr = false;
@@ -1316,10 +1373,42 @@ void conduit_step(cudaStream_t st, Family& F, const Level& L, const ConduitCoefs
     CK(cudaFuncSetAttribute(k_conduit_step_w<D, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr = true;
   }
-  const dim3 grid((F.maxitems + WPB - 1) / WPB, (unsigned)F.hs.size());
+  // persistent CTAs (the 48 KB of reference tables are built once per CTA): as many as fit on the GPU at once
+  static int ctas = 0;
+  if (!ctas) {
+    int per_sm = 0, dev = 0, nsm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conduit_step_w<D, WPB>, WPB * 32, sm));
+    ctas = std::max(1, per_sm) * nsm;
+  }
+  const int nbx = (F.maxitems + WPB - 1) / WPB, nsys = (int)F.hs.size();
+  // One CTA per block of WPB nodes; every CTA copies the prebuilt tables (49 KB, L2 hits) instead of building them
+  // (the per-CTA build from the reference tensors was 15% of the kernel's instructions).  Persistent CTAs
+  // (LPFEM_CSTEP_PERSIST=1, fine family on the main stream; LPFEM_CSTEP_TICKET=1: in-order block tickets) measured
+  // 74 -> 52 ms for the kernel, but the next fine step's GMRES got slower (cfg4 746 -> 845 ms per step): the
+  // persistent CTAs, each holding an SM's shared memory until the whole launch drains, delay the porous-stream kernels
+  // queued behind them, which then occupy the SMs the GMRES clusters are placed on.
+  static const int persist = getenv("LPFEM_CSTEP_PERSIST") ? atoi(getenv("LPFEM_CSTEP_PERSIST")) : 0;  // CTAs
+  static const bool use_ticket = getenv("LPFEM_CSTEP_TICKET") != nullptr;
+  const bool persistent = fine_main && persist > 0;
+  if (!c->cstab) {  // the kernel's reference tables, built once (k_cstep_tables), copied by every CTA
+    constexpr int tb = cstep_tab_bytes<D>();
+    c->cstab = dalloc<double>(tb / 8);
+    CK(cudaFuncSetAttribute(k_cstep_tables<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, tb));
+    k_cstep_tables<D><<<1, 512, tb, st>>>(refp<D>(c), c->cstab);
+    CKL();
+    CK(cudaStreamSynchronize(st));  // once: later launches on any stream read the tables
+  }
+  const int grid = (int)std::min<long long>((long long)nbx * nsys, persistent ? std::min(ctas, persist) : (1LL << 30));
+  if (persistent && use_ticket) {
+    if (!F.ticket) F.ticket = dalloc<int>(1);
+    CK(cudaMemsetAsync(F.ticket, 0, sizeof(int), st));
+  }
   k_conduit_step_w<D, WPB><<<grid, WPB * 32, sm, st>>>(F.ds, L, cc, newton, c->kmult, c->nc_p[0], c->nc_p[1], c->nc_p[2],
                                                       refp<D>(c), F.rowptr, F.col, F.aconst, colscale, F.z, F.W, F.lag,
-                                                      F.qf, F.aux, F.aout, F.rhs);
+                                                      F.qf, F.aux, F.aout, F.rhs, nbx, nsys,
+                                                      persistent && use_ticket ? F.ticket : nullptr, c->cstab);
   CKL();
 }
 
@@ -1386,7 +1475,10 @@ void coarse_box_inverses(lpfem_ctx* c, const double* cu_new, int slot) {
       CK(cudaStreamWaitEvent(st, c->einv[k], 0));
     }
   }
-  k_inv_rowmajor<float><<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, cm, c->ainv[slot]);
+  if (c->ainvb[slot])
+    k_inv_rowmajor<__nv_bfloat16><<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, cm, c->ainvb[slot]);
+  else
+    k_inv_rowmajor<float><<<dim3(F.maxrows, ns), 128, 0, st>>>(F.ds, F.mask, c->daoff, cm, c->ainv[slot]);
   CKL();
 }
 
@@ -1437,11 +1529,12 @@ void conduit_solve_once(lpfem_ctx* c, int lev, double t, const double* cu_new, c
   if (ml) {  // coarse-box inverses built by coarse_step (coarse stream, one step ahead)
     c->ml_busy = c->ml_next;
     c->ml.acif = c->ainv[c->ml_busy];
+    c->ml.acib = c->ainvb[c->ml_busy];
     c->ml.aci = nullptr;
   }
   double* colscale = ml ? C.mask : C.scale;  // ML: masked unscaled operator, M^-1 applied in the kernel
   const int newton = lev == 1 ? 1 : c->coarse_newton;
-  conduit_step<D>(st, C, c->Lc[lev], cc, newton, c, colscale);
+  conduit_step<D>(st, C, c->Lc[lev], cc, newton, c, colscale, lev == 1 && st == c->st);
   if (C.aout32) {
     k_round_f32<<<(unsigned)std::min<long long>((C.nnz + 255) / 256, 148 * 16), 256, 0, st>>>(C.aout, C.aout32, C.nnz);
     CKL();
@@ -1951,6 +2044,9 @@ void setup(lpfem_ctx* c) {
       if (lev == 1 && k == 1 && use_nb) build_nb<D>(c, F);
       // 2D: an fp32 copy of the CSR values for the Arnoldi products of the multilevel GMRES (LPFEM_NB_F64=1: none)
       if (lev == 1 && k == 1 && !use_nb && !getenv("LPFEM_NB_F64")) F.aout32 = dalloc<float>(F.nnz);
+      // fine porous: fp32 copy of the operators for the PCG's products, with true-residual replacement (experiment
+      // LPFEM_PCG_F32=1; measured: +4% / +9% PCG iterations at cfg4 / cfg2 for the same PCG time, so off)
+      if (lev == 1 && k == 0 && getenv("LPFEM_PCG_F32")) F.val32 = dalloc<float>(3 * F.nnz);
     }
   // multilevel preconditioner of the fine conduit systems: nested levels r h (r = 2, 4, .. dividing R)
   // and the coarse box at H (mlprec.cuh).  Requires the boxes to lie on coarse grid lines.
@@ -2059,6 +2155,10 @@ void setup(lpfem_ctx* c) {
       c->abuf = dalloc<double>(atot);
       c->ainv[0] = dalloc<float>(atot);
       c->ainv[1] = dalloc<float>(atot);
+      if (getenv("LPFEM_ML_BF16")) {
+        c->ainvb[0] = dalloc<__nv_bfloat16>(atot);
+        c->ainvb[1] = dalloc<__nv_bfloat16>(atot);
+      }
       c->gjperm = dalloc<int>(atot);
       c->dpoff = dalloc<long long>(poff.size());
       c->daoff = dalloc<long long>(aoff.size());
@@ -2256,6 +2356,14 @@ void setup(lpfem_ctx* c) {
     CK(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi));
     CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
+    if (const char* gs = getenv("LPFEM_GM_SPLIT")) {
+      if (sscanf(gs, "%d:%d:%d", &c->gm_split[0], &c->gm_split[1], &c->gm_split[2]) == 3 && c->gm_split[0] > 0) {
+        CK(cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->evs[i], cudaEventDisableTiming));
+      } else {
+        c->gm_split[0] = 0;
+      }
+    }
     {
       auto on = [](const char* k) { return getenv(k) != nullptr; };
       c->kn.verbose = on("LPFEM_VERBOSE");
@@ -2268,6 +2376,7 @@ void setup(lpfem_ctx* c) {
       c->kn.no_overlap = on("LPFEM_NO_OVERLAP");
       if (on("LPFEM_REORTH2")) c->kn.reorth2 = atof(getenv("LPFEM_REORTH2"));
       if (on("LPFEM_GJ_MAX")) c->kn.gj_max = atoi(getenv("LPFEM_GJ_MAX"));
+      if (on("LPFEM_PCG_RR")) c->kn.pcg_rr_fac = atof(getenv("LPFEM_PCG_RR"));
     }
     if (getenv("LPFEM_COARSE_PICARD")) c->coarse_newton = 0;
     if (getenv("LPFEM_VEL_W")) c->vw = atof(getenv("LPFEM_VEL_W"));      // experiment knobs
@@ -3007,14 +3116,15 @@ lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, dou
     int tpr = family == 0 ? (c->D == 2 ? 4 : 8) : (c->D == 2 ? TPR2 : TPR3);
     if (family == 1 && F.nbval) {  // the node-blocked operator the GMRES multiplies with
       // the values the GMRES's Arnoldi products read: the fp32 copy when there is one
-      const NBMat B{F.nbval, F.nbval32, F.nbcol, F.nbvptr, F.nbcptr, F.nblen};
+      const NBMat B{F.nbval, F.nbval32, F.nbcol, F.nbvptr, F.nbcptr, F.nblen, F.nbcol16, F.nbcbase};
       int maxi = 0;
       double bytes = 0.0;
       for (size_t i = 0; i < F.hk.size(); ++i) {
         const KSys& K = F.hk[i];
         maxi = std::max(maxi, K.n2 + K.n1);
       }
-      bytes = (F.nbval32 ? 4.0 : 8.0) * F.nnz + 4.0 * F.nb_ncols + 24.0 * F.nb_items + 16.0 * F.rows;
+      bytes = (F.nbval32 ? 4.0 : 8.0) * F.nnz + (F.nbcol16 ? 2.0 * F.nb_ncols + 8.0 * F.nb_items : 4.0 * F.nb_ncols) +
+              24.0 * F.nb_items + 16.0 * F.rows;
       const int ipc = 4 * NT / tpr;
       const dim3 grid((maxi + ipc - 1) / ipc, (unsigned)F.hk.size());
       void* fb = nullptr;
@@ -3195,7 +3305,7 @@ void lpfem_destroy(lpfem_ctx* c) {
   if (c->st3) cudaStreamSynchronize(c->st3);
   {
     void* mp[] = {c->gjperm, c->gjperm_p, c->pds3, c->part, c->aci, c->abuf, c->lwk, c->dpoff, c->daoff, c->lpiv, c->linfo,
-                  c->ainv[0], c->ainv[1], c->lwk2, c->lpiv2, c->linfo2};
+                  c->ainv[0], c->ainv[1], c->ainvb[0], c->ainvb[1], c->cstab, c->lwk2, c->lpiv2, c->linfo2};
     for (void* p : mp)
       if (p) cudaFree(p);
   }
@@ -3216,6 +3326,9 @@ void lpfem_destroy(lpfem_ctx* c) {
     cudaStreamDestroy(c->st2);
   }
   if (c->st3) cudaStreamDestroy(c->st3);
+  if (c->st4) cudaStreamDestroy(c->st4);
+  for (auto e : c->evs)
+    if (e) cudaEventDestroy(e);
   for (int i = 0; i < 3; ++i)
     if (c->evp[i]) cudaEventDestroy(c->evp[i]);
   for (int i = 0; i < 3; ++i)

@@ -27,6 +27,7 @@ struct MLArgs {
   const double* aci;            // dense inverses of the coarse-level systems (row-major), at aoff[sid]
   const float* acif;            // same stored in fp32 (conduit): the preconditioner is then a different but
                                 // fixed linear operator; right-preconditioned GMRES still meets C19 exactly
+  const __nv_bfloat16* acib;    // experiment (LPFEM_ML_BF16): the same in bf16 (used instead of acif when set)
   const long long* aoff;
   const SysDesc* fsys;          // fine boxes
   const double* s0;             // fine scaling (0 on fixed rows)
@@ -449,6 +450,11 @@ __global__ void __launch_bounds__(NT) k_gj_inverse(const SysDesc* __restrict__ s
 
 // row-major copy of the column-major inverses with the rows and columns of fixed DOFs zeroed
 template <class T>
+__device__ __forceinline__ T inv_cvt(double v) { return (T)v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 inv_cvt<__nv_bfloat16>(double v) { return __double2bfloat16(v); }
+
+template <class T>
 __global__ void k_inv_rowmajor(const SysDesc* __restrict__ sys, const double* __restrict__ mask,
                                const long long* __restrict__ aoff, const double* __restrict__ Acm,
                                T* __restrict__ Arm) {
@@ -460,7 +466,7 @@ __global__ void k_inv_rowmajor(const SysDesc* __restrict__ sys, const double* __
   T* dst = Arm + aoff[blockIdx.y] + (long long)i * n;
   const bool fi = mask[S.row_off + i] == 0.0;
   for (int j = threadIdx.x; j < n; j += blockDim.x)
-    dst[j] = (T)((fi || mask[S.row_off + j] == 0.0) ? 0.0 : src[(long long)j * n + i]);
+    dst[j] = inv_cvt<T>((fi || mask[S.row_off + j] == 0.0) ? 0.0 : src[(long long)j * n + i]);
 }
 
 __global__ void k_set_identity(const SysDesc* __restrict__ sys, const long long* __restrict__ aoff,
