@@ -33,6 +33,9 @@ namespace cgx = cooperative_groups;
 #ifndef LPFEM_BASIS_F32
 #define LPFEM_BASIS_F32 1
 #endif
+#ifndef LPFEM_ZW_F32
+#define LPFEM_ZW_F32 0
+#endif
 #ifndef LPFEM_NB_COLFIRST
 #define LPFEM_NB_COLFIRST 1
 #endif
@@ -431,9 +434,9 @@ __device__ __forceinline__ void spmv(const CtaPattern& P, const double* __restri
 // y = A x over the items [i0, i1) of one system (node-blocked format), TPR lanes per item; y rows of node i are
 // a n2 + i, of vertex k: D n2 + k.  The lanes of an item walk its neighbours; per neighbour one column load, D
 // (node) x gathers and D^2 value loads, all independent.
-template <int NT, int TPR, int D, class MT = double, bool C16 = false>
+template <int NT, int TPR, int D, class MT = double, bool C16 = false, class XT = double>
 __device__ __forceinline__ void spmv_nb(const NBMat& B, const MT* __restrict__ vals, long long item_off, int n2,
-                                        const double* __restrict__ x, double* __restrict__ y, int i0, int i1) {
+                                        const XT* __restrict__ x, double* __restrict__ y, int i0, int i1) {
   constexpr int NG = NT / TPR;
   const int lane = threadIdx.x % TPR;
   for (int base = i0; base < i1; base += NG) {
@@ -473,7 +476,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, const MT* __restrict__ v
 #pragma unroll
               for (int bb = 0; bb < D; ++bb) vv[a][bb] = (double)ldm(v + a * rl + bb * L + k);
 #pragma unroll
-            for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
+            for (int bb = 0; bb < D; ++bb) xb[bb] = (double)x[bb * n2 + c];
 #pragma unroll
             for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -489,7 +492,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, const MT* __restrict__ v
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) vv[a][bb] = (double)ldm(v + a * rl + bb * L + k);
 #pragma unroll
-          for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
+          for (int bb = 0; bb < D; ++bb) xb[bb] = (double)x[bb * n2 + c];
 #pragma unroll
           for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -501,7 +504,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, const MT* __restrict__ v
           double vv[D];
 #pragma unroll
           for (int a = 0; a < D; ++a) vv[a] = (double)ldm(v + a * rl + D * L + k);
-          const double xp = x[D * n2 + c];
+          const double xp = (double)x[D * n2 + c];
 #pragma unroll
           for (int a = 0; a < D; ++a) acc[a] += vv[a] * xp;
         }
@@ -512,7 +515,7 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, const MT* __restrict__ v
 #pragma unroll
           for (int bb = 0; bb < D; ++bb) vv[bb] = (double)ldm(v + bb * L + k);
 #pragma unroll
-          for (int bb = 0; bb < D; ++bb) xb[bb] = x[bb * n2 + c];
+          for (int bb = 0; bb < D; ++bb) xb[bb] = (double)x[bb * n2 + c];
 #pragma unroll
           for (int bb = 0; bb < D; ++bb) acc[0] += vv[bb] * xb[bb];
         }
@@ -553,9 +556,9 @@ __host__ __device__ constexpr int gmres_h_bytes(int M) { return (((M + 1) * M * 
 
 // Standalone batched SpMV over every system of a family (lpfem_bench_spmv): the Krylov kernels' row routine,
 // grid (row blocks, systems).
-template <int NT, int TPR, int PIPE_U>
+template <int NT, int TPR, int PIPE_U, class MT = double>
 __global__ void __launch_bounds__(NT) k_spmv_family(const KSys* __restrict__ sys, const long long* __restrict__ rowptr,
-                                                    const int* __restrict__ col, const double* __restrict__ val,
+                                                    const int* __restrict__ col, const MT* __restrict__ val,
                                                     const double* __restrict__ x, double* __restrict__ y,
                                                     int rows_per_cta) {
   const KSys K = sys[blockIdx.y];
@@ -563,10 +566,10 @@ __global__ void __launch_bounds__(NT) k_spmv_family(const KSys* __restrict__ sys
   if (r0 >= K.nrows) return;
   const int r1 = min(K.nrows, r0 + rows_per_cta);
   if (PIPE_U > 0)
-    spmv_rows_pipe<NT, TPR, (PIPE_U > 0 ? PIPE_U : 1)>(rowptr + K.prow_off, col, val + K.val_off, x + K.row_off,
-                                                      y + K.row_off, r0, r1);
+    spmv_rows_pipe<NT, TPR, (PIPE_U > 0 ? PIPE_U : 1), MT>(rowptr + K.prow_off, col, val + K.val_off, x + K.row_off,
+                                                          y + K.row_off, r0, r1);
   else
-    spmv_rows<NT, TPR>(rowptr + K.prow_off, col, val + K.val_off, x + K.row_off, y + K.row_off, r0, r1);
+    spmv_rows<NT, TPR, MT>(rowptr + K.prow_off, col, val + K.val_off, x + K.row_off, y + K.row_off, r0, r1);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -686,8 +689,8 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
 #endif
 constexpr int RLN = LPFEM_RLN;  // lanes per restricted row (4 vs 8: cfg2 GMRES 160 -> 153 ms, cfg1/cfg3 equal)
 
-template <int D, int NC, class VIN = double>
-__device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, double* __restrict__ Z, int r0,
+template <int D, int NC, class VIN = double, class ZT = double>
+__device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, ZT* __restrict__ Z, int r0,
                            int r1, int nrows) {
 #ifdef LPFEM_PHASE_TIMERS
   long long tsub = clock64();
@@ -837,7 +840,7 @@ __device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, 
         }
       }
     }
-    Z[i] = zi;
+    Z[i] = (ZT)zi;
   }
   (void)nrows;
 }
@@ -1221,7 +1224,22 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       if (j == 0) cl.sync();
       PHASE(0);
       const double sj = sig[j];
-      if constexpr (PC) {
+      if constexpr (PC && LPFEM_ZW_F32 && D == 3) {
+        // experiment: the preconditioned vector of the Arnoldi product in fp32 (node-blocked 3D only)
+        if (nbk && A.nb.val32) {
+          float* Zw32 = reinterpret_cast<float*>(Zw);
+          apply_prec<D, D, VT, float>(P, sid, V + j * ld, Zw32, r0, r1, K.nrows);
+          cl.sync();
+          PHASE(1);
+          spmv_nb<NT, TPR, D, float, false, float>(A.nb, A.nb.val32, K.item_off, K.n2, Zw32, W, it0, it1);
+          cl.sync();
+        } else {
+          apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
+          cl.sync();
+          PHASE(1);
+          matvec(Zw, W, true);
+        }
+      } else if constexpr (PC) {
         apply_prec<D, D>(P, sid, V + j * ld, Zw, r0, r1, K.nrows);
         cl.sync();
         PHASE(1);

@@ -3167,7 +3167,7 @@ lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, dou
       const KSys& K = F.hk[i];
       maxr = std::max(maxr, K.nrows);
       const double nz = (double)(F.hrp[K.prow_off + K.nrows] - F.hrp[K.prow_off]);
-      bytes += 12.0 * nz + 8.0 * (K.nrows + 1) + 16.0 * K.nrows;
+      bytes += (family == 1 && F.aout32 ? 8.0 : 12.0) * nz + 8.0 * (K.nrows + 1) + 16.0 * K.nrows;
     }
     const dim3 grid((maxr + rpc - 1) / rpc, (unsigned)F.hk.size());
     void* fb = nullptr;
@@ -3182,7 +3182,11 @@ lpfem_status lpfem_bench_spmv(lpfem_ctx* c, int family, int reps, int flush, dou
       CK(cudaEventRecord(e0, c->st));
       // the Krylov kernels' choice: pipelined rows (U = 4) for the porous family and the 2D conduit, plain 3D conduit
       const int pu = getenv("LPFEM_SPMV_PIPE") ? atoi(getenv("LPFEM_SPMV_PIPE")) : (family == 0 || c->D == 2 ? 4 : 0);
-#define LP_SPMV(T, P) k_spmv_family<NT, T, P><<<grid, NT, 0, c->st>>>(F.dk, F.rowptr, F.col, val, x, y, rpc)
+      // (the 2D conduit: the fp32 values the GMRES's Arnoldi products read)
+#define LP_SPMV(T, P)                                                                                            \
+  ((family == 1 && F.aout32)                                                                                     \
+       ? k_spmv_family<NT, T, P, float><<<grid, NT, 0, c->st>>>(F.dk, F.rowptr, F.col, F.aout32, x, y, rpc)     \
+       : k_spmv_family<NT, T, P><<<grid, NT, 0, c->st>>>(F.dk, F.rowptr, F.col, val, x, y, rpc))
       if (pu == 4) {
         if (tpr == 4) LP_SPMV(4, 4);
         else if (tpr == 8) LP_SPMV(8, 4);
