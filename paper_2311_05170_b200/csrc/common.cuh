@@ -107,6 +107,17 @@ HD void unlex(long long r, const int* shape, int l[3]) {
   }
 }
 
+// 32-bit overload: row and node indices inside one box fit an int, and a 64-bit division by a runtime divisor is a
+// ~70-instruction subroutine (the preconditioner's transfers unlex every row of every Krylov iteration)
+template <int D>
+HD void unlex(int r, const int* shape, int l[3]) {
+  for (int a = 0; a < D; ++a) {
+    const int q = r / shape[a];
+    l[a] = r - q * shape[a];
+    r = q;
+  }
+}
+
 template <int D>
 HD long long lex(const int l[3], const int* shape) {
   long long r = 0, s = 1;

@@ -747,11 +747,12 @@ __device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, 
       const SysDesc SC = P.lsys[l][bx];
       double* dst = LRp(l);
       const int wfirst = (gt & ~31) / RLN;  // warp-uniform trip count (shuffles inside)
-      for (int it = gt / RLN, w0 = wfirst; w0 < SC.nrows; it += gs / RLN, w0 += gs / RLN) {
+      const int nitems = SC.nrows - (NC - 1) * SC.n2;  // a node's NC components in one item
+      for (int it = gt / RLN, w0 = wfirst; w0 < nitems; it += gs / RLN, w0 += gs / RLN) {
         if (l == 0)
-          restrict_item<D, NC, RLN>(SF, SC, P.st[l], v, dst, it, gt % RLN);
+          restrict_node<D, NC, RLN>(SF, SC, P.st[l], v, dst, it, gt % RLN);
         else
-          restrict_item<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
+          restrict_node<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
       }
       SUBPHASE(2 * l);
       cl.sync();
@@ -818,13 +819,64 @@ __device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, 
         const double* sl = LSp(l);
         const double* zu = LZp(l + 1);
         double* zl = LZp(l);
-        for (int i = gt; i < SL.nrows; i += gs) zl[i] = sl[i] * rl[i] + prolong_row<D, NC>(SL, SU, P.q[l + 1], zu, i);
+        // velocity nodes (NC components per item), then the P1 rows
+        const int nitems = SL.nrows - (NC - 1) * SL.n2;
+        for (int it = gt; it < nitems; it += gs) {
+          if (it < SL.n2) {
+            double pz[NC];
+            prolong_node<D, NC>(SL, SU, P.q[l + 1], zu, it, pz);
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+              const int i = k * SL.n2 + it;
+              zl[i] = sl[i] * rl[i] + pz[k];
+            }
+          } else {
+            const int i = it + (NC - 1) * SL.n2;
+            zl[i] = sl[i] * rl[i] + prolong_row<D, NC>(SL, SU, P.q[l + 1], zu, i);
+          }
+        }
         cl.sync();
       }
     }
   }
   SUBPHASE(7);
   const double* s0 = P.s0 + f * P.fstride + S0.row_off;
+  if (NC > 1 && P.direct == 0) {
+    // fine combine over the whole cluster, a node's NC velocity components per item (one location / weight
+    // evaluation for all of them), then the P1 rows; Z is complete after the caller's cluster barrier
+    const int nitems = S0.nrows - (NC - 1) * S0.n2;
+    for (int it = gt; it < nitems; it += gs) {
+      if (it < S0.n2) {
+        double si[NC], zi[NC];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          si[k] = s0[k * S0.n2 + it];
+          zi[k] = si[k] != 0.0 ? si[k] * (double)v[k * S0.n2 + it] : 0.0;
+          any = any || si[k] != 0.0;
+        }
+        if (P.nl > 0 && any) {
+          double pz[NC];
+          prolong_node<D, NC>(S0, P.lsys[0][bx], P.q[0], LZp(0), it, pz);
+#pragma unroll
+          for (int k = 0; k < NC; ++k)
+            if (si[k] != 0.0) zi[k] += pz[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) Z[k * S0.n2 + it] = (ZT)zi[k];
+      } else {
+        const int i = it + (NC - 1) * S0.n2;
+        const double si = s0[i];
+        double zi = 0.0;
+        if (si != 0.0) {
+          zi = si * (double)v[i];
+          if (P.nl > 0) zi += prolong_row<D, NC>(S0, P.lsys[0][bx], P.q[0], LZp(0), i);
+        }
+        Z[i] = (ZT)zi;
+      }
+    }
+    return;
+  }
   for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
     const double si = s0[i];
     double zi = 0.0;
@@ -1348,6 +1400,7 @@ __global__ void __launch_bounds__(NT, 1) k_gmres(KArgs A, MLArgs P) {
       for (int i = r0 + tid; i < r1; i += NT) r[i] = basis_comb(V, ld, yv, jend, i);
       cl.sync();
       apply_prec<D, D>(P, sid, r, Zw, r0, r1, K.nrows);
+      cl.sync();  // the fine combine writes Z over the whole cluster
       for (int i = r0 + tid; i < r1; i += NT) x[i] += Zw[i];
     } else {
       for (int i = r0 + tid; i < r1; i += NT) x[i] += basis_comb(V, ld, yv, jend, i);

@@ -277,6 +277,116 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
   if (valid && lane == 0) dst[row] = s0;
 }
 
+// restrict_item with the NC velocity components of a node in one item: items 0..SC.n2-1 are the coarse P2 nodes
+// (class-major), items SC.n2.. the P1 vertices.  The stencil walk (class, offsets, clipping, index arithmetic) is
+// shared by the components; every component's sum is the same ordered sum as restrict_item's (bitwise equal).
+template <int D, int NC, int LN, class ST>
+__device__ __forceinline__ void restrict_node(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
+                                              const ST* __restrict__ src, double* __restrict__ dst, int item,
+                                              int lane) {
+  const int nitems = SC.nrows - (NC - 1) * SC.n2;
+  const bool valid = item < nitems;
+  if (!valid) item = 0;
+  int l[3] = {0, 0, 0}, cls, row;
+  int shp[3];
+  const int q = T->q;
+  const bool vel = item < SC.n2;
+  const ST* sv;
+  if (vel) {
+    int rem = item;
+    cls = 0;
+    for (; cls < (1 << D); ++cls) {
+      int cnt = 1;
+      for (int a = 0; a < D; ++a) cnt *= SC.nc[a] + 1 - ((cls >> a) & 1);
+      if (rem < cnt) break;
+      rem -= cnt;
+    }
+    int ext[3] = {1, 1, 1};
+    for (int a = 0; a < D; ++a) ext[a] = SC.nc[a] + 1 - ((cls >> a) & 1);
+    int i3[3] = {0, 0, 0};
+    unlex<D>(rem, ext, i3);
+    for (int a = 0; a < D; ++a) l[a] = 2 * i3[a] + ((cls >> a) & 1);
+    row = (int)lex<D>(l, SC.np);
+    sv = src;
+    for (int a = 0; a < 3; ++a) shp[a] = SF.np[a];
+  } else {
+    const int shp1[3] = {SC.nc[0] + 1, SC.nc[1] + 1, SC.nc[2] + 1};
+    unlex<D>(item - SC.n2, shp1, l);
+    row = NC * SC.n2 + item - SC.n2;
+    for (int a = 0; a < D; ++a) l[a] *= 2;
+    cls = 8;
+    sv = src + (long long)NC * SF.n2;
+    for (int a = 0; a < 3; ++a) shp[a] = SF.nc[a] + 1;
+  }
+  const long long cs = vel ? SF.n2 : 0;  // component stride (P1 items read their one component NC times)
+  const int b = T->start[cls], e = b + T->len[cls];
+  const int sh = cls == 8 ? 1 : 0;
+  int base[3] = {0, 0, 0};
+  for (int a = 0; a < D; ++a) base[a] = q * l[a];
+  double s[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) s[k] = 0.0;
+#pragma unroll 2
+  for (int i = b + lane; valid && i < e; i += LN) {
+    int g0[3];
+    bool ok0 = true;
+    for (int a = 0; a < D; ++a) {
+      g0[a] = base[a] + T->off[i][a];
+      ok0 = ok0 && g0[a] >= 0 && g0[a] <= 2 * SF.nc[a];
+      g0[a] = min(max(g0[a], 0), 2 * SF.nc[a]) >> sh;
+    }
+    const long long id = lex<D>(g0, shp);
+    const double w = T->w[i];
+    double v[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) v[k] = (double)sv[k * cs + id];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) s[k] += ok0 ? w * v[k] : 0.0;
+  }
+#pragma unroll
+  for (int o = LN / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < NC; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o, LN);
+  if (valid && lane == 0) {
+    if (vel) {
+#pragma unroll
+      for (int k = 0; k < NC; ++k) dst[k * SC.n2 + row] = s[k];
+    } else {
+      dst[row] = s[0];
+    }
+  }
+}
+
+// prolong_row for the NC velocity components of fine node nd at once (one location and weight evaluation for all
+// components; each component's sum in prolong_row's order, bitwise equal)
+template <int D, int NC>
+__device__ __forceinline__ void prolong_node(const SysDesc& SF, const SysDesc& SC, int q, const double* __restrict__ src,
+                                             int nd, double out[NC]) {
+  int g[3] = {0, 0, 0}, cell[3];
+  unlex<D>(nd, SF.np, g);
+  int code[n2_of(D)];
+  double w[n2_of(D)];
+  p2_weights<D>(g, q, SC.nc, cell, code, w);
+  int id[n2_of(D)];
+#pragma unroll
+  for (int n = 0; n < n2_of(D); ++n) {
+    int l[3];
+    code_point<D>(code[n], cell, l);
+    id[n] = (int)lex<D>(l, SC.np);
+  }
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    double v[n2_of(D)];
+#pragma unroll
+    for (int n = 0; n < n2_of(D); ++n) v[n] = src[k * SC.n2 + id[n]];
+    double s = 0.0;
+#pragma unroll
+    for (int n = 0; n < n2_of(D); ++n)
+      if (w[n] != 0.0) s += w[n] * v[n];
+    out[k] = s;
+  }
+}
+
 // prolongation of a coarser-level vector src (box SC) to row `row` of the finer level box SF (ratio q)
 template <int D, int NC>
 __device__ __forceinline__ double prolong_row(const SysDesc& SF, const SysDesc& SC, int q,
