@@ -277,6 +277,11 @@ __device__ __forceinline__ void restrict_item(const SysDesc& SF, const SysDesc& 
   if (valid && lane == 0) dst[row] = s0;
 }
 
+#ifndef LPFEM_RUNROLL
+#define LPFEM_RUNROLL 2
+#endif
+constexpr int RUNROLL = LPFEM_RUNROLL;  // stencil entries per lane in flight in restrict_node
+
 // restrict_item with the NC velocity components of a node in one item: items 0..SC.n2-1 are the coarse P2 nodes
 // (class-major), items SC.n2.. the P1 vertices.  The stencil walk (class, offsets, clipping, index arithmetic) is
 // shared by the components; every component's sum is the same ordered sum as restrict_item's (bitwise equal).
@@ -326,7 +331,7 @@ __device__ __forceinline__ void restrict_node(const SysDesc& SF, const SysDesc& 
   double s[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) s[k] = 0.0;
-#pragma unroll 2
+#pragma unroll RUNROLL
   for (int i = b + lane; valid && i < e; i += LN) {
     int g0[3];
     bool ok0 = true;
