@@ -689,6 +689,16 @@ __global__ void __launch_bounds__(NT, 1) k_cg(KArgs A) {
 #endif
 constexpr int RLN = LPFEM_RLN;  // lanes per restricted row (4 vs 8: cfg2 GMRES 160 -> 153 ms, cfg1/cfg3 equal)
 
+// all items of one level restriction, LN lanes per item, over the cluster's threads (gt of gs)
+template <int D, int NC, int LN, class ST>
+__device__ __forceinline__ void restrict_level(const SysDesc& SF, const SysDesc& SC, const Stencil* __restrict__ T,
+                                               const ST* __restrict__ src, double* __restrict__ dst, int nitems,
+                                               int gt, int gs) {
+  const int wfirst = (gt & ~31) / LN;  // warp-uniform trip count (shuffles inside)
+  for (int it = gt / LN, w0 = wfirst; w0 < nitems; it += gs / LN, w0 += gs / LN)
+    restrict_node<D, NC, LN>(SF, SC, T, src, dst, it, gt % LN);
+}
+
 template <int D, int NC, class VIN = double, class ZT = double>
 __device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, ZT* __restrict__ Z, int r0,
                            int r1, int nrows) {
@@ -746,13 +756,15 @@ __device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, 
     for (int l = 0; l < P.nl; ++l) {
       const SysDesc SC = P.lsys[l][bx];
       double* dst = LRp(l);
-      const int wfirst = (gt & ~31) / RLN;  // warp-uniform trip count (shuffles inside)
       const int nitems = SC.nrows - (NC - 1) * SC.n2;  // a node's NC components in one item
-      for (int it = gt / RLN, w0 = wfirst; w0 < nitems; it += gs / RLN, w0 += gs / RLN) {
-        if (l == 0)
-          restrict_node<D, NC, RLN>(SF, SC, P.st[l], v, dst, it, gt % RLN);
-        else
-          restrict_node<D, NC, RLN>(SF, SC, P.st[l], src, dst, it, gt % RLN);
+      if (l == 0) {
+        restrict_level<D, NC, RLN>(SF, SC, P.st[l], v, dst, nitems, gt, gs);
+      } else if (nitems * RLN * 2 <= gs) {
+        // few items with long stencils (the coarse box, ratio H / (2h)): a warp per item, so that every thread
+        // of the cluster walks a part of a stencil (RLN lanes per item left most threads idle)
+        restrict_level<D, NC, 32>(SF, SC, P.st[l], src, dst, nitems, gt, gs);
+      } else {
+        restrict_level<D, NC, RLN>(SF, SC, P.st[l], src, dst, nitems, gt, gs);
       }
       SUBPHASE(2 * l);
       cl.sync();
@@ -778,13 +790,32 @@ __device__ void apply_prec(const MLArgs& P, int sid, const VIN* __restrict__ v, 
         if (lane == 0) zc[i] = s;
       }
     } else if (P.acif) {
+      // CR rows per warp at once (CR independent row streams in flight per lane; rc[j] loaded once for all of
+      // them); each row's sum in the same order as one row per warp
+      constexpr int CR = 4;
       const float* Ai = P.acif + P.aoff[sid];
-      for (int i = gt >> 5; i < n; i += gs >> 5) {
-        double s = 0.0;
-#pragma unroll 4
-        for (int j = lane; j < n; j += 32) s += (double)Ai[(long long)i * n + j] * rc[j];
-        s = warp_sum(s);
-        if (lane == 0) zc[i] = s;
+      for (int i0 = (gt >> 5) * CR; i0 < n; i0 += (gs >> 5) * CR) {
+        double s[CR];
+        const float* Ar[CR];
+#pragma unroll
+        for (int c = 0; c < CR; ++c) {
+          s[c] = 0.0;
+          Ar[c] = Ai + (long long)min(i0 + c, n - 1) * n;  // rows past n repeat the last row (not stored)
+        }
+#pragma unroll 2
+        for (int j = lane; j < n; j += 32) {
+          const double rj = rc[j];
+          float a[CR];
+#pragma unroll
+          for (int c = 0; c < CR; ++c) a[c] = Ar[c][j];
+#pragma unroll
+          for (int c = 0; c < CR; ++c) s[c] += (double)a[c] * rj;
+        }
+#pragma unroll
+        for (int c = 0; c < CR; ++c) {
+          const double t = warp_sum(s[c]);
+          if (lane == 0 && i0 + c < n) zc[i0 + c] = t;
+        }
       }
     } else {
       const double* Ai = P.aci + P.aoff[sid];
