@@ -36,6 +36,9 @@ namespace cgx = cooperative_groups;
 #ifndef LPFEM_ZW_F32
 #define LPFEM_ZW_F32 0
 #endif
+#ifndef LPFEM_DOT16
+#define LPFEM_DOT16 0
+#endif
 #ifndef LPFEM_NB_COLFIRST
 #define LPFEM_NB_COLFIRST 1
 #endif
@@ -1105,6 +1108,46 @@ __device__ __forceinline__ void dots_chunked(RedSmem<NT, NV>& S, const VT* __res
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const bool up4 = lane & 4, up2 = lane & 2, up1 = lane & 1;
+#if LPFEM_DOT16
+  // experiment: 16 basis vectors per pass, one row per round (the same 16 loads in flight; w read half as often)
+  const bool up8 = lane & 8;
+  for (int c0 = 0; c0 < nk; c0 += 16) {
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+    double ww = 0.0;
+    for (int i = r0 + threadIdx.x; i < r1; i += NT) {
+      const double wi = ws * (double)w[i];
+      VT va[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) va[u] = Vt[min(c0 + u, nk - 1) * ld + i];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u] += c0 + u < nk ? (double)va[u] * wi : 0.0;
+      ww += wi * wi;
+    }
+    if (pww && c0 == 0) *pww += ww;
+    double a8[8], a4[4], a2[2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double send = up8 ? acc[u] : acc[u + 8];
+      a8[u] = (up8 ? acc[u + 8] : acc[u]) + __shfl_xor_sync(FULL, send, 8);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double send = up4 ? a8[u] : a8[u + 4];
+      a4[u] = (up4 ? a8[u + 4] : a8[u]) + __shfl_xor_sync(FULL, send, 4);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double send = up2 ? a4[u] : a4[u + 2];
+      a2[u] = (up2 ? a4[u + 2] : a4[u]) + __shfl_xor_sync(FULL, send, 2);
+    }
+    double a1 = (up1 ? a2[1] : a2[0]) + __shfl_xor_sync(FULL, up1 ? a2[0] : a2[1], 1);
+    a1 += __shfl_xor_sync(FULL, a1, 16);
+    if (lane < 16 && c0 + lane < nk) S.red[threadIdx.x >> 5][k0 + c0 + lane] = a1;
+  }
+  return;
+#endif
   for (int c0 = 0; c0 < nk; c0 += 8) {
     double acc[8];
 #pragma unroll

@@ -291,6 +291,7 @@ struct lpfem_ctx {
   struct Knobs {
     bool verbose = false, no_smem_pattern = false, cold_start = false, coarse_full_newton = false;
     bool no_concurrent = false, no_alg1_fastpath = false, no_overlap = false;
+    bool pcg_ungated = false;  // experiment: the porous PCG launches without waiting for the GMRES launch
     double reorth2 = 0.1;
     int gj_max = 512;
     double pcg_rr_fac = 1e-10;  // mixed-precision PCG: true-residual replacement when ||r||^2 fell by this factor
@@ -1352,7 +1353,7 @@ void porous_stage(lpfem_ctx* c, int lev, double t, double* const* cnew, double* 
                                                              c->nc_p[2], refp<D>(c), P.z, P.lag, P.qf, P.aux, P.isq,
                                                              P.rhs, P.wn, P.rows);
   CKL();
-  if (lev == 1 && c->gate) CK(cudaStreamWaitEvent(st, c->evp[2], 0));  // the GMRES clusters are placed first
+  if (lev == 1 && c->gate && !c->kn.pcg_ungated) CK(cudaStreamWaitEvent(st, c->evp[2], 0));  // the GMRES clusters are placed first
   if (lev == 1) CK(cudaEventRecord(c->ek[0], st));
   solve_porous<D>(c, P);
   if (lev == 1) CK(cudaEventRecord(c->ek[1], st));
@@ -2372,6 +2373,7 @@ void setup(lpfem_ctx* c) {
       c->kn.cold_start = on("LPFEM_COLD_START");
       c->kn.coarse_full_newton = on("LPFEM_COARSE_FULL_NEWTON");
       c->kn.no_concurrent = on("LPFEM_NO_CONCURRENT");
+      c->kn.pcg_ungated = on("LPFEM_PCG_UNGATED");
       c->kn.no_alg1_fastpath = on("LPFEM_NO_ALG1_FASTPATH");
       c->kn.no_overlap = on("LPFEM_NO_OVERLAP");
       if (on("LPFEM_REORTH2")) c->kn.reorth2 = atof(getenv("LPFEM_REORTH2"));
