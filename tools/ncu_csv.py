@@ -1,6 +1,6 @@
 """Summarise an ncu raw-page CSV (ncu -i REP --page raw --csv): key metrics per kernel launch.
 
-    python tools_ncu_csv.py gpurun_out/NAME_raw.csv [kernel-substring] [min-ms]
+    python tools/ncu_csv.py gpurun_out/NAME_raw.csv [kernel-substring] [min-ms]
 """
 import csv
 import sys
@@ -66,7 +66,7 @@ def record(path, kernel, workload, out_txt, desc, min_ms=0.0):
         wr = float(r[h.index("dram__bytes_write.sum")]) * sc[u[h.index("dram__bytes_write.sum")]]
         tot += rd + wr
         n += 1
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    tpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     traffic[f"{kernel}@{workload}"] = {"dram_bytes_per_launch": tot / max(n, 1), "source": os.path.basename(out_txt),
                                         "what": desc}

@@ -1,5 +1,5 @@
 """Aggregate ncu source-page stall samples and executed instructions per CUDA source line.
-    python tools_ncu_lines.py report.ncu-rep [topN]"""
+    python tools/ncu_lines.py report.ncu-rep [topN]"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],

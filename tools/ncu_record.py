@@ -1,7 +1,7 @@
 """Record an ncu --set full report under profiles/: key metrics per kernel launch (text) and, for bench.py's
 roofline, the DRAM traffic per launch of each kernel (profiles/ncu_traffic.json).
 
-    python tools_ncu_record.py gpurun_out/prof.ncu-rep profiles/r01_ncu_gmres_cfg1.txt "description" cfg1
+    python tools/ncu_record.py gpurun_out/prof.ncu-rep profiles/r01_ncu_gmres_cfg1.txt "description" cfg1
 """
 import csv
 import io

@@ -1,4 +1,4 @@
-"""One config, a few steps (for ncu captures): python tools_profile_step.py CFG STEPS"""
+"""One config, a few steps (for ncu captures): python tools/profile_step.py CFG STEPS"""
 import sys
 sys.path.insert(0, '.')
 import lpfem_inputs as I
