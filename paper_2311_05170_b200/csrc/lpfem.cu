@@ -2355,7 +2355,12 @@ void setup(lpfem_ctx* c) {
     if (getenv("LPFEM_NO_PRIO")) prio_hi = prio_lo;
     c->prio_hi = prio_hi;
     CK(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio_hi));
-    CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+    // experiment (LPFEM_PCG_PRIO): the porous stream one priority level above the caller's stream, so that SMs a
+    // finished GMRES cluster frees go to waiting PCG CTAs before waiting GMRES clusters (default: equal priority)
+    if (getenv("LPFEM_PCG_PRIO") && prio_hi < prio_lo)
+      CK(cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking, std::min(prio_lo - 1, std::max(prio_hi + 1, prio_lo - atoi(getenv("LPFEM_PCG_PRIO"))))));
+    else
+      CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
     if (const char* gs = getenv("LPFEM_GM_SPLIT")) {
       if (sscanf(gs, "%d:%d:%d", &c->gm_split[0], &c->gm_split[1], &c->gm_split[2]) == 3 && c->gm_split[0] > 0) {
