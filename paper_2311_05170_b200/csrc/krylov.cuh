@@ -36,6 +36,9 @@ namespace cgx = cooperative_groups;
 #ifndef LPFEM_ZW_F32
 #define LPFEM_ZW_F32 0
 #endif
+#ifndef LPFEM_NB_PREFETCH
+#define LPFEM_NB_PREFETCH 0  // experiment: node-blocked SpMV, L2 bulk prefetch this many rounds ahead
+#endif
 #ifndef LPFEM_DOT16
 #define LPFEM_DOT16 0
 #endif
@@ -444,6 +447,28 @@ __device__ __forceinline__ void spmv_nb(const NBMat& B, const MT* __restrict__ v
   const int lane = threadIdx.x % TPR;
   for (int base = i0; base < i1; base += NG) {
     const int it = base + threadIdx.x / TPR;
+#if LPFEM_NB_PREFETCH
+    // experiment: lane 0 of an item's group asks the L2 for the values and columns of the item this group takes
+    // LPFEM_NB_PREFETCH rounds ahead (bulk prefetch: no registers or shared memory held while in flight).  The
+    // range is widened to 16-byte bounds; the last item of the CTA's range is skipped so that the widened end stays
+    // inside the next item's data.
+    if (!C16 && lane == 0) {
+      const int itp = it + LPFEM_NB_PREFETCH * NG;
+      if (itp + 1 < i1) {
+        const long long gp = item_off + itp;
+        const int2 lp = B.len[gp];
+        const bool nd = itp < n2;
+        const unsigned long long v0 = (unsigned long long)(vals + B.vptr[gp]);
+        const unsigned long long v1 = v0 + sizeof(MT) * (size_t)(nd ? D * (D * lp.x + lp.y) : D * lp.x);
+        const unsigned long long c0 = (unsigned long long)(B.col + B.cptr[gp]);
+        const unsigned long long c1 = c0 + 4ull * (size_t)(nd ? lp.x + lp.y : lp.x);
+        const unsigned long long va = v0 & ~15ull, ca = c0 & ~15ull;
+        const unsigned vb = (unsigned)(((v1 + 15ull) & ~15ull) - va), cbb = (unsigned)(((c1 + 15ull) & ~15ull) - ca);
+        if (vb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(va), "r"(vb) : "memory");
+        if (cbb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ca), "r"(cbb) : "memory");
+      }
+    }
+#endif
     double acc[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) acc[a] = 0.0;
