@@ -13,7 +13,12 @@ import pytest
 import protocol_norms as PN
 
 pytestmark = pytest.mark.gpu
-LEVELS = (0, 1, 2)
+# Levels run: h = 1/4, 1/16 by default (20 s on a B200); LPFEM_PROTOCOL_LEVELS=0,1,2 adds h = 1/64 (4096 steps per
+# scheme, +3.5 min), the run whose table is committed as profiles/r02_protocol_ex1_th.json (DESIGN 7).
+LEVELS = tuple(int(x) for x in os.environ.get("LPFEM_PROTOCOL_LEVELS", "0,1").split(","))
+# porous columns of Algorithm 3 against Algorithm 1's at the finest level run: within 2x at h = 1/64; at h = 1/16
+# the coarse term H^3 = 1/64 still shows in |||p_m|||_0 (measured 3.0x), so the bound there is 3.5x
+POROUS_FACTOR = {1: 3.5, 2: 2.0}
 
 
 @pytest.fixture(scope="module")
@@ -63,11 +68,12 @@ def test_local_parallel_against_the_traditional_scheme(runs):
     """T1 vs T2 with Taylor-Hood elements.  Theorem P:1478-1494 bounds Algorithm 3's error by
     Delta t + h^r + H^(r+1) (times 1 + Delta t^(-1/2) in H1); with r = 2 and the paper's scaling h = H^2 the coarse
     term H^3 = h^1.5 exceeds Algorithm 1's h^2, so only the porous errors are expected to match Algorithm 1's at the
-    finest level (the paper's MINI/P1 has r = 1, where H^2 = h matches): porous columns within 2x of Algorithm 1's;
+    finest level (the paper's MINI/P1 has r = 1, where H^2 = h matches): porous columns within 2x of Algorithm 1's
+    at h = 1/64 (3.5x at h = 1/16, POROUS_FACTOR);
     the velocity gap |||u|||_1(Alg 3) - |||u|||_1(Alg 1) shrinks from level to level."""
     lev = LEVELS[-1]
     for k in COLS[1:]:
-        assert runs[(3, lev)][k] <= 2.0 * runs[(1, lev)][k], (lev, k, runs[(3, lev)][k], runs[(1, lev)][k])
+        assert runs[(3, lev)][k] <= POROUS_FACTOR[lev] * runs[(1, lev)][k], (lev, k, runs[(3, lev)][k], runs[(1, lev)][k])
     gaps = [runs[(3, l)]["u_1"] - runs[(1, l)]["u_1"] for l in LEVELS]
     print("velocity H1 gap Alg3 - Alg1 per level", gaps)
     assert all(b < a for a, b in zip(gaps[:-1], gaps[1:])), gaps
